@@ -1,0 +1,243 @@
+"""CPU oracle for Machine Learning Sort (arXiv 1805.04272) -- TEST INFRASTRUCTURE.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s `cpu_baseline` /
+`--impl reference` legs may import this package.  The product package
+`paper_1805_04272_b200` never imports it, and the two share no code; the only
+common dependency is the seeded input generator module `workloads/`.
+
+The arithmetic lives in `mlsort_oracle.c` (plain C, fp64, -ffp-contract=off),
+one function per step of the paper's algorithm, each citing its passage; this
+file only marshals numpy arrays through ctypes.  `sorted_reference` and
+`select_sorted` are the plain definition of the result (a stable sort under
+IEEE totalOrder) written with numpy library routines.
+
+Parity pins (tests/test_oracle_pins.py) check every function here against what
+the paper and the mathematics fix; see DESIGN.md "Oracle and pins".
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "mlsort_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+ORACLE_ERR_NONFINITE = 5
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (no fast-math, no FMA contraction)."""
+    if force or not os.path.exists(_LIB_PATH) or \
+            os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
+                               "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = C.CDLL(_LIB_PATH)
+        d, u64, i64, u32, i = C.c_double, C.c_uint64, C.c_int64, C.c_uint32, C.c_int
+        P = C.c_void_p
+        lib.oracle_validate.argtypes = [P, u64]
+        lib.oracle_validate.restype = i64
+        lib.oracle_gvm_forward.argtypes = [i, P, P, P, P, d, d, d]
+        lib.oracle_gvm_forward.restype = d
+        lib.oracle_predict.argtypes = [i, P, P, P, P, d, d, P, u64, P]
+        lib.oracle_predict.restype = None
+        lib.oracle_bucket_of.argtypes = [d, u64]
+        lib.oracle_bucket_of.restype = u64
+        lib.oracle_bucket.argtypes = [P, u64, u64, P]
+        lib.oracle_bucket.restype = None
+        lib.oracle_place_fixup.argtypes = [P, P, u64, u64, P, P, P, P]
+        lib.oracle_place_fixup.restype = i
+        lib.oracle_verify_repair.argtypes = [P, P, u64, i]
+        lib.oracle_verify_repair.restype = u64
+        lib.oracle_tails.argtypes = [P, u64, d, d, P, P]
+        lib.oracle_tails.restype = None
+        lib.oracle_ml_sort.argtypes = [P, u64, i, P, P, P, P, d, d, u64, i, P, P, P, P, P, P]
+        lib.oracle_ml_sort.restype = i
+        lib.oracle_expected_occupancy.argtypes = [u64, u64, u64]
+        lib.oracle_expected_occupancy.restype = d
+        lib.oracle_occupancy_histogram.argtypes = [P, u64, u32, P]
+        lib.oracle_occupancy_histogram.restype = None
+        _lib = lib
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _weights(w: dict):
+    m = int(w["m"])
+    arrs = [np.ascontiguousarray(np.asarray(w[k], dtype=np.float64)) for k in ("w1", "w2", "b", "beta")]
+    for a in arrs:
+        assert a.shape == (m,)
+    return m, arrs, float(w["input_lo"]), float(w["input_hi"])
+
+
+def _as_f64(keys):
+    return np.ascontiguousarray(np.asarray(keys).astype(np.float64, copy=False))
+
+
+class NonFiniteKey(ValueError):
+    def __init__(self, index):
+        super().__init__(f"non-finite key at index {index}")
+        self.index = index
+
+
+def validate(keys) -> int:
+    """Lowest index of a NaN/Inf key, or -1 (step 1)."""
+    x = _as_f64(keys)
+    return int(_load().oracle_validate(_ptr(x), x.shape[0]))
+
+
+def gvm_forward(w: dict, x: float) -> float:
+    """Eq. 3 for a single key (§2 l.73-76)."""
+    m, (w1, w2, b, beta), lo, hi = _weights(w)
+    return float(_load().oracle_gvm_forward(m, _ptr(w1), _ptr(w2), _ptr(b), _ptr(beta), lo, hi, float(x)))
+
+
+def predict(w: dict, keys) -> np.ndarray:
+    """Eq. 3 for every key, fp64 (step 2)."""
+    m, (w1, w2, b, beta), lo, hi = _weights(w)
+    x = _as_f64(keys)
+    y = np.empty(x.shape[0], dtype=np.float64)
+    _load().oracle_predict(m, _ptr(w1), _ptr(w2), _ptr(b), _ptr(beta), lo, hi, _ptr(x), x.shape[0], _ptr(y))
+    return y
+
+
+def bucket_of(y: float, B: int) -> int:
+    """r = round(y*B) half away from zero, clamped to [0, B-1] (step 3)."""
+    return int(_load().oracle_bucket_of(float(y), int(B)))
+
+
+def bucket(y, B: int) -> np.ndarray:
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.float64))
+    out = np.empty(y.shape[0], dtype=np.uint32)
+    _load().oracle_bucket(_ptr(y), y.shape[0], int(B), _ptr(out))
+    return out
+
+
+def place_fixup(keys, buckets, B: int):
+    """Steps 5-7 with given bucket ids: returns (sorted keys f64, idx u32, counts u32, moves)."""
+    x = _as_f64(keys)
+    bk = np.ascontiguousarray(np.asarray(buckets, dtype=np.uint32))
+    n = x.shape[0]
+    ok = np.empty(n, dtype=np.float64)
+    oi = np.empty(n, dtype=np.uint32)
+    cnt = np.empty(int(B), dtype=np.uint32)
+    mv = np.zeros(1, dtype=np.uint64)
+    rc = _load().oracle_place_fixup(_ptr(x), _ptr(bk), n, int(B), _ptr(ok), _ptr(oi), _ptr(cnt), _ptr(mv))
+    if rc:
+        raise MemoryError("oracle_place_fixup")
+    return ok, oi, cnt, int(mv[0])
+
+
+def verify_repair(keys, idx, stable: bool = True):
+    """Step 8 on copies: returns (keys, idx, violations_before_repair)."""
+    k = _as_f64(keys).copy()
+    i = np.ascontiguousarray(np.asarray(idx, dtype=np.uint32)).copy()
+    bad = _load().oracle_verify_repair(_ptr(k), _ptr(i), k.shape[0], 1 if stable else 0)
+    return k, i, int(bad)
+
+
+def tails(keys, lo: float, hi: float):
+    x = _as_f64(keys)
+    a = np.zeros(1, dtype=np.uint64)
+    b = np.zeros(1, dtype=np.uint64)
+    _load().oracle_tails(_ptr(x), x.shape[0], float(lo), float(hi), _ptr(a), _ptr(b))
+    return int(a[0]), int(b[0])
+
+
+def ml_sort(keys, w: dict, B: int = 0, stable: bool = True, want_y: bool = False,
+            want_buckets: bool = False, want_counts: bool = False) -> dict:
+    """Full pipeline, steps 1-9.  Returns dict with keys (same dtype as input), perm
+    (uint32, gather form), optional y, buckets, counts, and diagnostics."""
+    keys = np.asarray(keys)
+    x = _as_f64(keys)
+    n = x.shape[0]
+    B = int(B) if B else n
+    m, (w1, w2, b, beta), lo, hi = _weights(w)
+    ok = np.empty(n, dtype=np.float64)
+    oi = np.empty(n, dtype=np.uint32)
+    y = np.empty(n, dtype=np.float64) if want_y else None
+    bk = np.empty(n, dtype=np.uint32) if want_buckets else None
+    cnt = np.empty(max(B, 1), dtype=np.uint32) if want_counts else None
+    info = np.zeros(6, dtype=np.int64)
+    rc = _load().oracle_ml_sort(_ptr(x), n, m, _ptr(w1), _ptr(w2), _ptr(b), _ptr(beta), lo, hi, B,
+                                1 if stable else 0, _ptr(ok), _ptr(oi), _ptr(y), _ptr(bk), _ptr(cnt),
+                                _ptr(info))
+    if rc == ORACLE_ERR_NONFINITE:
+        raise NonFiniteKey(int(info[0]))
+    if rc:
+        raise MemoryError("oracle_ml_sort")
+    out = {"keys": ok.astype(keys.dtype) if keys.dtype != np.float64 else ok, "perm": oi,
+           "repairs": int(info[1]), "tail_lo": int(info[2]), "tail_hi": int(info[3]),
+           "fixup_moves": int(info[4]), "max_bucket": int(info[5])}
+    if want_y:
+        out["y"] = y
+    if want_buckets:
+        out["buckets"] = bk
+    if want_counts:
+        out["counts"] = cnt[:B] if n else np.zeros(B, dtype=np.uint32)
+    return out
+
+
+def expected_occupancy(N: int, B: int, q: int) -> float:
+    """Eq. 5, Binomial(N, 1/B) (reading A8)."""
+    return float(_load().oracle_expected_occupancy(int(N), int(B), int(q)))
+
+
+def occupancy_histogram(counts, qmax: int = 8) -> np.ndarray:
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.uint32))
+    h = np.zeros(qmax + 1, dtype=np.uint64)
+    _load().oracle_occupancy_histogram(_ptr(c), c.shape[0], int(qmax), _ptr(h))
+    return h
+
+
+# ---- the plain definition of the result: stable sort under totalOrder
+
+def order_bits(keys) -> np.ndarray:
+    """IEEE-754 totalOrder as unsigned integers (reading A10)."""
+    keys = np.asarray(keys)
+    if keys.dtype == np.float32:
+        u = keys.view(np.uint32)
+        return np.where(u >> 31, ~u, u | np.uint32(0x80000000)).astype(np.uint32)
+    u = keys.astype(np.float64, copy=False).view(np.uint64)
+    return np.where(u >> 63, ~u, u | np.uint64(0x8000000000000000)).astype(np.uint64)
+
+
+def sorted_reference(keys):
+    """(sorted keys, perm) = stable sort of (key, index) under totalOrder."""
+    ob = order_bits(keys)
+    perm = np.argsort(ob, kind="stable").astype(np.uint32)
+    return np.asarray(keys)[perm], perm
+
+
+def select_sorted(keys, positions, stable: bool = True):
+    """Sampled outputs of the sorted result without sorting everything: for each position p,
+    the p-th smallest key and (stable) the input index of the p-th element of the stable
+    order.  O(N) per position."""
+    keys = np.asarray(keys)
+    ob = order_bits(keys)
+    out_k, out_i = [], []
+    for p in positions:
+        p = int(p)
+        v = np.partition(ob, p)[p]
+        less = int(np.count_nonzero(ob < v))
+        eq = np.flatnonzero(ob == v)
+        i = int(eq[p - less])
+        out_k.append(keys[i])
+        out_i.append(i)
+    return np.array(out_k, dtype=keys.dtype), np.array(out_i, dtype=np.int64)
