@@ -1,0 +1,105 @@
+// common.cuh -- device helpers shared by the libmlsort kernels (sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mlsort {
+
+constexpr int kThreads = 512;            // threads per CTA for K1 / K3
+constexpr int kWarps = kThreads / 32;
+
+// Device-side status word written by the kernels and read once per sort.
+struct DevStatus {
+    unsigned long long bad_index;   // lowest non-finite key index (ULLONG_MAX = none)
+    unsigned long long tail_lo;     // keys < input_lo
+    unsigned long long tail_hi;     // keys > input_hi
+    unsigned long long violations;  // adjacent order violations found by the verify pass
+    unsigned long long big_count;   // coarse buckets routed to the overflow path
+    unsigned long long big_elems;   // elements in those buckets
+    unsigned long long max_coarse;  // largest coarse bucket
+    unsigned long long overflow;    // internal capacity overflow (must be 0)
+    unsigned long long ticket;      // dynamic CTA ticket for the ordered K3 look-back
+    unsigned long long pad[7];
+};
+
+// ---- IEEE-754 totalOrder as unsigned integers (reading A10): negative -> ~bits,
+// non-negative -> bits | sign.  Equal order bits <=> bit-identical keys.
+template <typename K> struct KeyTraits;
+template <> struct KeyTraits<float> {
+    using Bits = uint32_t;
+    __device__ __forceinline__ static Bits to_ord(float x) {
+        uint32_t u = __float_as_uint(x);
+        return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    }
+    __device__ __forceinline__ static float from_ord(Bits o) {
+        return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+    }
+    __device__ __forceinline__ static bool finite(float x) {
+        return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u;
+    }
+};
+template <> struct KeyTraits<double> {
+    using Bits = unsigned long long;
+    __device__ __forceinline__ static Bits to_ord(double x) {
+        unsigned long long u = (unsigned long long)__double_as_longlong(x);
+        return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+    }
+    __device__ __forceinline__ static double from_ord(Bits o) {
+        return __longlong_as_double((long long)((o >> 63) ? (o & 0x7fffffffffffffffull) : ~o));
+    }
+    __device__ __forceinline__ static bool finite(double x) {
+        return ((unsigned long long)__double_as_longlong(x) & 0x7ff0000000000000ull) !=
+               0x7ff0000000000000ull;
+    }
+};
+
+// ---- block-wide exclusive scan of one uint32 per thread (NT threads).
+// `scratch` needs NT/32 + 1 words of shared memory.  Returns the exclusive prefix;
+// *total receives the block sum.  Contains two __syncthreads().
+template <int NT>
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* scratch,
+                                                         uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) scratch[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < NT / 32 ? scratch[lane] : 0u;
+        uint32_t s = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < NT / 32) scratch[lane] = s - w;
+        if (lane == NT / 32 - 1) scratch[NT / 32] = s;
+    }
+    __syncthreads();
+    uint32_t excl = scratch[warp] + x - v;
+    *total = scratch[NT / 32];
+    return excl;
+}
+
+template <int NT>
+__device__ __forceinline__ uint32_t block_reduce_sum(uint32_t v, uint32_t* scratch) {
+    uint32_t t;
+    block_exclusive_scan<NT>(v, scratch, &t);
+    return t;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+}  // namespace mlsort

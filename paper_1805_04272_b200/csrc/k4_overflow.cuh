@@ -1,0 +1,280 @@
+// k4_overflow.cuh -- K4 overflow path, K5 boundary verify, and the conventional-sort
+// fallback (a stable LSD radix sort).
+//
+// The paper sorts the keys that its model cannot place well with "conventional sorting
+// algorithms (like Quick Sort)" (§3 l.121, tails) and SPEC escalates to a full
+// comparison sort when verification fails.  Here a coarse bucket too large
+// for K3's distributed shared memory (heavy duplicates, e.g. BASELINE C5, or a skewed
+// model) is first gathered in tile order with each tile's piece sorted by input index, so
+// the gathered run is in input order; an all-equal run is then already final (stable
+// copy-through), otherwise a stable LSD radix sort by key finishes it.  The same radix
+// sort, applied to the whole input, is the fallback when the verify pass finds a
+// violation (non-monotone weights, reading A14).
+#pragma once
+
+#include "common.cuh"
+#include "k3_sort.cuh"
+
+namespace mlsort {
+
+// ------------------------------------------------------------------ K4 gather
+// Persistent CTAs take big coarse buckets from big_list.  flags[k]: bit0 all keys equal,
+// bit1 run is in input order (every piece was small enough to sort by index).
+template <typename KeyT, bool PERM>
+__global__ void __launch_bounds__(kK3Threads, 1)
+k4_big_gather(uint32_t num_tiles, uint32_t R, const KeyT* __restrict__ part_keys,
+              const uint16_t* __restrict__ part_fine, const uint32_t* __restrict__ part_idx,
+              const uint16_t* __restrict__ matrix, const unsigned long long* __restrict__ starts,
+              KeyT* __restrict__ out_keys, uint32_t* __restrict__ out_perm,
+              unsigned long long* __restrict__ range_start, DevStatus* __restrict__ st,
+              const uint32_t* __restrict__ big_list, uint32_t* __restrict__ flags,
+              unsigned long long* __restrict__ ticket) {
+    using Bits = typename KeyTraits<KeyT>::Bits;
+    __shared__ uint32_t scratch[64];
+    __shared__ unsigned long long s_round;
+    __shared__ uint32_t s_k;
+    __shared__ int s_unordered;
+    __shared__ unsigned long long s_min, s_max;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned long long nbig = st->big_count;
+    (void)part_fine;
+    while (true) {
+        if (tid == 0) s_k = (uint32_t)atomicAdd(ticket, 1ull);
+        __syncthreads();
+        const uint32_t k = s_k;
+        if (k >= nbig) return;
+        const uint32_t c = big_list[k];
+        const unsigned long long S0 = starts[c];
+        if (tid == 0) {
+            s_round = S0;
+            s_unordered = 0;
+            s_min = ~0ull;
+            s_max = 0ull;
+            range_start[(size_t)c * R] = S0;
+        }
+        Bits vmin = ~(Bits)0, vmax = 0;
+        __syncthreads();
+        const uint16_t* colc = matrix + (size_t)c * num_tiles;
+        const uint16_t* colc1 = matrix + (size_t)(c + 1) * num_tiles;
+        for (uint32_t tr = 0; tr < num_tiles; tr += kK3Threads) {
+            const uint32_t t = tr + warp * 32 + lane;
+            uint32_t off = 0, len = 0;
+            if (t < num_tiles) {
+                off = colc[t];
+                len = (uint32_t)colc1[t] - off;
+            }
+            uint32_t incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t excl = incl - len;
+            const uint32_t wtotal = __shfl_sync(0xffffffffu, incl, 31);
+            uint32_t rtotal;
+            const uint32_t wbase = block_exclusive_scan<kK3Threads>(lane == 31 ? wtotal : 0u, scratch, &rtotal);
+            const unsigned long long base = s_round + __shfl_sync(0xffffffffu, wbase, 31);
+            for (uint32_t b0 = 0; b0 < wtotal; b0 += 32) {
+                const uint32_t i = b0 + lane;
+                int lo = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int cand = lo + step;
+                    const uint32_t v = __shfl_sync(0xffffffffu, excl, cand & 31);
+                    if (cand < 32 && v <= i) lo = cand;
+                }
+                const uint32_t poff = __shfl_sync(0xffffffffu, off, lo);
+                const uint32_t pexc = __shfl_sync(0xffffffffu, excl, lo);
+                if (i < wtotal) {
+                    const size_t src = (size_t)(tr + warp * 32 + lo) * kTileK3 + poff + (i - pexc);
+                    const KeyT key = part_keys[src];
+                    const Bits ob = KeyTraits<KeyT>::to_ord(key);
+                    vmin = ob < vmin ? ob : vmin;
+                    vmax = ob > vmax ? ob : vmax;
+                    out_keys[base + i] = key;
+                    if (PERM) out_perm[base + i] = part_idx[src];
+                }
+            }
+            if (PERM) {   // each piece comes from one tile (one input-index range): sort it by index
+                __syncwarp();
+                if (len > 64) {
+                    s_unordered = 1;
+                } else if (len > 1) {
+                    const unsigned long long s = base + excl;
+                    for (uint32_t a = 1; a < len; ++a) {
+                        const KeyT kv = out_keys[s + a];
+                        const uint32_t iv = out_perm[s + a];
+                        uint32_t j = a;
+                        while (j > 0 && out_perm[s + j - 1] > iv) {
+                            out_keys[s + j] = out_keys[s + j - 1];
+                            out_perm[s + j] = out_perm[s + j - 1];
+                            --j;
+                        }
+                        out_keys[s + j] = kv;
+                        out_perm[s + j] = iv;
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid == 0) s_round += rtotal;
+            __syncthreads();
+        }
+        // all-equal test
+        if (vmin != ~(Bits)0) {
+            atomicMin(&s_min, (unsigned long long)vmin);
+            atomicMax(&s_max, (unsigned long long)vmax);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const bool equal = (s_min == s_max);
+            flags[k] = (equal ? 1u : 0u) | (s_unordered ? 0u : 2u);
+            if (!equal || (PERM && s_unordered)) atomicAdd(&st->overflow, 1ull);   // needs K4 radix
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ K5 boundary verify
+// Every K3 slice / K4 run recorded its output start; check the pair that straddles it.
+template <typename KeyT, bool PERM>
+__global__ void k5_boundary_verify(const unsigned long long* __restrict__ range_start, uint64_t num,
+                                   const KeyT* __restrict__ out_keys, const uint32_t* __restrict__ out_perm,
+                                   DevStatus* __restrict__ st) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= num) return;
+    const unsigned long long s = range_start[i];
+    if (s == ~0ull || s == 0) return;
+    const auto a = KeyTraits<KeyT>::to_ord(out_keys[s - 1]);
+    const auto b = KeyTraits<KeyT>::to_ord(out_keys[s]);
+    const bool ok = PERM ? precedes<KeyT, true>(a, out_perm[s - 1], b, out_perm[s]) : (a <= b);
+    if (!ok) atomicAdd(&st->violations, 1ull);
+}
+
+// ------------------------------------------------------------------ LSD radix sort (stable)
+constexpr int kRadixThreads = 512;
+constexpr int kRadixItems = 16;
+constexpr int kRadixChunk = kRadixThreads * kRadixItems;   // 8192
+
+template <typename KeyT>
+__global__ void k_to_ord(const KeyT* __restrict__ in, typename KeyTraits<KeyT>::Bits* __restrict__ out,
+                         uint32_t* __restrict__ iota, uint64_t n, uint64_t iota_base) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        out[i] = KeyTraits<KeyT>::to_ord(in[i]);
+        if (iota) iota[i] = (uint32_t)(iota_base + i);
+    }
+}
+template <typename KeyT>
+__global__ void k_from_ord(const typename KeyTraits<KeyT>::Bits* __restrict__ in, KeyT* __restrict__ out,
+                           uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = KeyTraits<KeyT>::from_ord(in[i]);
+}
+
+// digit of element: from the key bits (field 0) or from the 32-bit payload (field 1)
+template <typename Bits>
+__device__ __forceinline__ uint32_t radix_digit(Bits k, uint32_t v, int field, int shift) {
+    return field == 0 ? (uint32_t)((k >> shift) & 255u) : ((v >> shift) & 255u);
+}
+
+template <typename Bits>
+__global__ void __launch_bounds__(kRadixThreads)
+k_radix_hist(const Bits* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t n, int field,
+             int shift, uint32_t nchunks, uint32_t* __restrict__ ghist) {
+    __shared__ uint32_t h[256];
+    for (int i = threadIdx.x; i < 256; i += kRadixThreads) h[i] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)blockIdx.x * kRadixChunk;
+    for (int k = 0; k < kRadixItems; ++k) {
+        const uint64_t e = base + threadIdx.x + (uint64_t)k * kRadixThreads;
+        if (e < n) atomicAdd(&h[radix_digit<Bits>(keys[e], vals ? vals[e] : 0u, field, shift)], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < 256; d += kRadixThreads) ghist[(size_t)d * nchunks + blockIdx.x] = h[d];
+}
+
+// in-place exclusive scan of m entries with one CTA (digit-major order)
+__global__ void __launch_bounds__(1024) k_radix_scan(uint32_t* __restrict__ a, uint64_t m) {
+    __shared__ uint32_t scratch[64];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const uint64_t per = 16;
+    for (uint64_t b = 0; b < m; b += 1024 * per) {
+        const uint64_t s = b + threadIdx.x * per;
+        uint32_t local = 0;
+        for (uint64_t i = s; i < min(m, s + per); ++i) local += a[i];
+        uint32_t total;
+        uint32_t run = block_exclusive_scan<1024>(local, scratch, &total) + carry;
+        for (uint64_t i = s; i < min(m, s + per); ++i) {
+            const uint32_t v = a[i];
+            a[i] = run;
+            run += v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry += total;
+        __syncthreads();
+    }
+}
+
+// Stable scatter: warp w owns elements [w*512, (w+1)*512) of the chunk, processed in lane order.
+template <typename Bits>
+__global__ void __launch_bounds__(kRadixThreads)
+k_radix_scatter(const Bits* __restrict__ kin, const uint32_t* __restrict__ vin, Bits* __restrict__ kout,
+                uint32_t* __restrict__ vout, uint64_t n, int field, int shift, uint32_t nchunks,
+                const uint32_t* __restrict__ ghist) {
+    constexpr int W = kRadixThreads / 32;
+    __shared__ uint16_t wcnt[W][256];
+    __shared__ uint32_t goff[256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < W * 256; i += kRadixThreads) (&wcnt[0][0])[i] = 0;
+    for (int d = threadIdx.x; d < 256; d += kRadixThreads) goff[d] = ghist[(size_t)d * nchunks + blockIdx.x];
+    __syncthreads();
+    const uint64_t base = (uint64_t)blockIdx.x * kRadixChunk + (uint64_t)warp * 32 * kRadixItems;
+    Bits k[kRadixItems];
+    uint32_t v[kRadixItems], rank[kRadixItems], dig[kRadixItems];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < kRadixItems; ++r) {
+        const uint64_t e = base + (uint64_t)r * 32 + lane;
+        const bool ok = e < n;
+        k[r] = ok ? kin[e] : (Bits)0;
+        v[r] = (ok && vin) ? vin[e] : 0u;
+        dig[r] = ok ? radix_digit<Bits>(k[r], v[r], field, shift) : 256u + lane;   // unique dummy
+        const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
+        const uint32_t before = ok ? wcnt[warp][dig[r]] : 0u;
+        rank[r] = before + __popc(peers & lt);
+        __syncwarp();
+        if (ok && (peers & lt) == 0) wcnt[warp][dig[r]] = (uint16_t)(before + __popc(peers));
+        __syncwarp();
+    }
+    __syncthreads();
+    // exclusive prefix over warps for each digit
+    for (int d = threadIdx.x; d < 256; d += kRadixThreads) {
+        uint32_t run = 0;
+        for (int w = 0; w < W; ++w) {
+            const uint32_t c = wcnt[w][d];
+            wcnt[w][d] = (uint16_t)run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRadixItems; ++r) {
+        const uint64_t e = base + (uint64_t)r * 32 + lane;
+        if (e < n) {
+            const uint64_t dst = (uint64_t)goff[dig[r]] + wcnt[warp][dig[r]] + rank[r];
+            kout[dst] = k[r];
+            if (vout) vout[dst] = v[r];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ misc
+template <typename KeyT>
+__global__ void k_gather_payload(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ payload,
+                                 uint32_t* __restrict__ out, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = payload[perm[i]];
+}
+
+}  // namespace mlsort

@@ -1,0 +1,787 @@
+// mlsort.cu -- libmlsort.so device entry points: plan selection, workspace layout, kernel
+// dispatch and the one host synchronisation per sort.
+//
+// Pipeline of mlsort_sort:
+//   K1 predict + bucket + tile partition      (Eq. 3 l.73-76, l.65)
+//   K2 coarse-bucket starts (column sums of the tile-offset matrix)
+//   K3 cluster gather + rank-bucket placement + per-bucket fix-up (l.86)
+//   K4 overflow path for coarse buckets K3 cannot hold (l.121 tails)
+//   K5 boundary verify (reading A14) -> conventional-sort fallback on violation
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+#include "common.cuh"
+#include "predict.cuh"
+#include "k1_partition.cuh"
+#include "k3_sort.cuh"
+#include "k4_overflow.cuh"
+#include "dist.cuh"
+
+using namespace mlsort;
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess) {                                                                \
+            fprintf(stderr, "mlsort: CUDA error %s at %s:%d: %s\n", cudaGetErrorName(e_),       \
+                    __FILE__, __LINE__, cudaGetErrorString(e_));                                \
+            return MLSORT_ERR_CUDA;                                                             \
+        }                                                                                       \
+    } while (0)
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr size_t kK3SmemBudget = 230400;     // 1 CTA per SM (1024 threads)
+constexpr int kSMs = 148;
+
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+inline uint32_t ceil_log2(uint64_t x) {
+    uint32_t r = 0;
+    while ((1ull << r) < x) ++r;
+    return r;
+}
+
+// ---------------------------------------------------------------- folded weights (A1 item 1)
+FoldedWeights fold(const Weights& w, uint32_t mpad) {
+    FoldedWeights f;
+    std::memset(&f, 0, sizeof(f));
+    const double log2e = 1.4426950408889634;
+    const double span = w.hi - w.lo;
+    for (uint32_t j = 0; j < mpad; ++j) {
+        if (j < w.m) {
+            f.A[j] = (float)(-2.0 * w.beta[j] * w.w1[j] * log2e / span);
+            f.C[j] = (float)(w.beta[j] * (w.w1[j] + w.b[j]) * log2e);
+            f.W[j] = (float)w.w2[j];
+        } else {
+            f.A[j] = 0.0f;
+            f.C[j] = 0.0f;
+            f.W[j] = 0.0f;   // pad neurons contribute nothing
+        }
+    }
+    return f;
+}
+
+uint32_t mpad_of(uint32_t m) { return m <= 16 ? 16 : m <= 32 ? 32 : 64; }
+
+// ---------------------------------------------------------------- plan
+struct Plan {
+    uint64_t n = 0, B = 0;
+    uint32_t T = 0, fb = 0, C = 0, R = 1, kr = 1, cap = 0;
+    size_t k1_smem = 0, k3_smem = 0;
+    size_t ks = 4;
+    bool perm = false;
+};
+
+size_t k3_elem_bytes(size_t ks, bool perm) { return ks * 2 + 2 + (perm ? 8 : 0); }
+
+Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm) {
+    Plan p;
+    p.n = n;
+    p.B = B;
+    p.ks = ks;
+    p.perm = perm;
+    p.T = (uint32_t)((n + kTile - 1) / kTile);
+    const size_t eb = k3_elem_bytes(ks, perm);
+    const uint32_t lb = ceil_log2(B);
+    const uint32_t fb_max = std::min<uint32_t>(16, lb);
+    const uint32_t fb_min = lb > 14 ? lb - 14 : 0;   // C <= 16384
+    bool found = false;
+    for (int fb = (int)fb_max; fb >= (int)fb_min && !found; --fb) {
+        const uint64_t C = (B + (1ull << fb) - 1) >> fb;
+        const size_t k1 = (size_t)C * 4 + (size_t)kTile * ks + (perm ? (size_t)kTile * 4 : 0) + kTile * 2 + 512;
+        if (k1 > 227 * 1024) continue;
+        const double avg = (double)n * (double)(1ull << fb) / (double)B;
+        for (uint32_t R = 1; R <= 8; R <<= 1) {
+            if ((1u << fb) < R) break;
+            const uint32_t kr = (1u << fb) / R;
+            if (kr > 16384) continue;
+            const long long capll = ((long long)kK3SmemBudget - 256 - 16 - 4ll * kr) / (long long)eb;
+            if (capll < 64) continue;
+            if (avg <= 0.55 * R * (double)capll) {
+                p.fb = (uint32_t)fb;
+                p.C = (uint32_t)C;
+                p.R = R;
+                p.kr = kr;
+                p.cap = (uint32_t)capll;
+                p.k1_smem = k1;
+                found = true;
+                break;
+            }
+        }
+    }
+    if (!found) {   // heavily skewed sizes: smallest coarse buckets K1 allows, overflow path does the rest
+        p.fb = fb_min > 16 ? 16 : std::max<uint32_t>(fb_min, std::min<uint32_t>(fb_max, 16));
+        p.C = (uint32_t)((B + (1ull << p.fb) - 1) >> p.fb);
+        p.R = (1u << p.fb) >= 8 ? 8 : (1u << p.fb);
+        p.kr = (1u << p.fb) / p.R;
+        p.cap = (uint32_t)(((long long)kK3SmemBudget - 256 - 16 - 4ll * p.kr) / (long long)eb);
+        p.k1_smem = (size_t)p.C * 4 + (size_t)kTile * ks + (perm ? (size_t)kTile * 4 : 0) + kTile * 2 + 512;
+    }
+    p.k3_smem = 256 + (size_t)p.cap * ks * 2 + (size_t)p.kr * 4 + (perm ? (size_t)p.cap * 8 : 0) + (size_t)p.cap * 2 + 16;
+    return p;
+}
+
+// ---------------------------------------------------------------- workspace layout
+struct Layout {
+    size_t status = 0, part_keys = 0, part_fine = 0, part_idx = 0, matrix = 0, starts = 0,
+           range_start = 0, big_list = 0, flags = 0, radix = 0, total = 0;
+    size_t radix_bytes = 0;
+};
+
+size_t radix_area(uint64_t n, size_t bits_bytes, bool payload) {
+    const uint64_t nchunks = (n + kRadixChunk - 1) / kRadixChunk;
+    return align_up(n * bits_bytes) * 2 + (payload ? align_up(n * 4) * 2 : 0) + align_up(nchunks * 256 * 4);
+}
+
+Layout make_layout(const Plan& p) {
+    Layout L;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += align_up(bytes);
+        return o;
+    };
+    L.status = take(sizeof(DevStatus));
+    // part_* (K1 -> K3/K4) and the radix area (K4 radix / fallback) are never live together
+    const size_t part_bytes = align_up(p.n * p.ks) + align_up(p.n * 2) + (p.perm ? align_up(p.n * 4) : 0);
+    const size_t rad = radix_area(p.n, p.ks, p.perm);
+    const size_t shared_area = std::max(part_bytes, rad);
+    const size_t area = take(shared_area);
+    L.part_keys = area;
+    L.part_fine = area + align_up(p.n * p.ks);
+    L.part_idx = L.part_fine + align_up(p.n * 2);
+    L.radix = area;
+    L.radix_bytes = shared_area;
+    L.matrix = take((size_t)(p.C + 1) * p.T * 2);
+    L.starts = take((size_t)(p.C + 1) * 8);
+    L.range_start = take((size_t)p.C * p.R * 8);
+    L.big_list = take((size_t)p.C * 4);
+    L.flags = take((size_t)p.C * 4);
+    L.total = off;
+    return L;
+}
+
+template <typename T>
+T* at(void* ws, size_t off) {
+    return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+struct HostStatusBuf {
+    DevStatus* h = nullptr;
+    std::mutex mu;
+};
+thread_local DevStatus* tl_status = nullptr;
+DevStatus* host_status() {
+    if (!tl_status) {
+        if (cudaMallocHost(&tl_status, sizeof(DevStatus)) != cudaSuccess) {
+            tl_status = nullptr;
+            static DevStatus fallback;
+            return &fallback;
+        }
+    }
+    return tl_status;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = kSMs;
+    }
+    return g_num_sms;
+}
+
+// ---------------------------------------------------------------- launch helpers
+struct Launches {
+    uint64_t count = 0;
+};
+
+template <typename KeyT, int MPAD, int PRED, bool PERM, bool GIVEN>
+cudaError_t launch_k1_t(const Plan& p, const KeyT* keys, const FoldedWeights& fw, const K1Params& kp,
+                        void* ws, const Layout& L, cudaStream_t s, const uint32_t* bucket_in,
+                        const uint32_t* idx_in, uint32_t b_lo) {
+    auto kern = k1_predict_partition<KeyT, MPAD, PRED, PERM, GIVEN>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k1_smem);
+    if (e != cudaSuccess) return e;
+    kern<<<p.T, kThreads, p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.part_keys), at<uint16_t>(ws, L.part_fine),
+                                          PERM ? at<uint32_t>(ws, L.part_idx) : nullptr,
+                                          at<uint16_t>(ws, L.matrix), at<DevStatus>(ws, L.status), bucket_in,
+                                          idx_in, b_lo);
+    return cudaGetLastError();
+}
+
+template <typename KeyT, bool PERM, bool GIVEN>
+cudaError_t launch_k1(const Plan& p, const KeyT* keys, uint32_t mpad, int pred, const FoldedWeights& fw,
+                      const K1Params& kp, void* ws, const Layout& L, cudaStream_t s,
+                      const uint32_t* bucket_in = nullptr, const uint32_t* idx_in = nullptr, uint32_t b_lo = 0) {
+    if (GIVEN) return launch_k1_t<KeyT, 16, kPredMufu, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo);
+#define K1CASE(M)                                                                                          \
+    if (mpad == M) {                                                                                       \
+        if (pred == kPredMufu)                                                                             \
+            return launch_k1_t<KeyT, M, kPredMufu, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo); \
+        return launch_k1_t<KeyT, M, kPredMixed, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo);    \
+    }
+    K1CASE(16) K1CASE(32) K1CASE(64)
+#undef K1CASE
+    return cudaErrorInvalidValue;
+}
+
+template <typename KeyT, bool PERM, int R>
+cudaError_t launch_k3_t(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm,
+                        cudaStream_t s) {
+    auto kern = k3_cluster_sort<KeyT, PERM, R>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k3_smem);
+    if (e != cudaSuccess) return e;
+    K3Params kp;
+    kp.num_tiles = p.T;
+    kp.num_coarse = p.C;
+    kp.owner_shift = p.fb - ceil_log2(p.R);
+    kp.kr = p.kr;
+    kp.cap = p.cap;
+    kp.pad = 0;
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(p.C * R);
+    cfg.blockDim = dim3(kK3Threads);
+    cfg.dynamicSmemBytes = p.k3_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = R;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, kp, (const KeyT*)at<KeyT>(ws, L.part_keys),
+                              (const uint16_t*)at<uint16_t>(ws, L.part_fine),
+                              (const uint32_t*)(PERM ? at<uint32_t>(ws, L.part_idx) : nullptr),
+                              (const uint16_t*)at<uint16_t>(ws, L.matrix),
+                              (const unsigned long long*)at<unsigned long long>(ws, L.starts), out_keys, out_perm,
+                              at<unsigned long long>(ws, L.range_start), at<DevStatus>(ws, L.status),
+                              at<uint32_t>(ws, L.big_list));
+}
+
+template <typename KeyT, bool PERM>
+cudaError_t launch_k3(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s) {
+    switch (p.R) {
+        case 1: return launch_k3_t<KeyT, PERM, 1>(p, ws, L, out_keys, out_perm, s);
+        case 2: return launch_k3_t<KeyT, PERM, 2>(p, ws, L, out_keys, out_perm, s);
+        case 4: return launch_k3_t<KeyT, PERM, 4>(p, ws, L, out_keys, out_perm, s);
+        case 8: return launch_k3_t<KeyT, PERM, 8>(p, ws, L, out_keys, out_perm, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+// Stable LSD radix sort of (ord bits, payload) pairs, n elements, in the radix area.
+// Passes over the payload digits first when `payload_first` (restores input order),
+// then over the key digits.  Returns the buffer index (0/1) holding the result.
+template <typename Bits>
+int radix_sort_pairs(Bits* k0, uint32_t* v0, Bits* k1, uint32_t* v1, uint32_t* ghist, uint64_t n,
+                     bool payload_first, cudaStream_t s, Launches& nl, cudaError_t& err) {
+    const uint32_t nchunks = (uint32_t)((n + kRadixChunk - 1) / kRadixChunk);
+    int cur = 0;
+    auto pass = [&](int field, int shift) {
+        Bits* ki = cur ? k1 : k0;
+        uint32_t* vi = cur ? v1 : v0;
+        Bits* ko = cur ? k0 : k1;
+        uint32_t* vo = cur ? v0 : v1;
+        k_radix_hist<Bits><<<nchunks, kRadixThreads, 0, s>>>(ki, vi, n, field, shift, nchunks, ghist);
+        k_radix_scan<<<1, 1024, 0, s>>>(ghist, (uint64_t)nchunks * 256);
+        k_radix_scatter<Bits><<<nchunks, kRadixThreads, 0, s>>>(ki, vi, ko, vo, n, field, shift, nchunks, ghist);
+        nl.count += 3;
+        cur ^= 1;
+    };
+    if (payload_first && v0)
+        for (int sh = 0; sh < 32; sh += 8) pass(1, sh);
+    for (int sh = 0; sh < (int)(sizeof(Bits) * 8); sh += 8) pass(0, sh);
+    err = cudaGetLastError();
+    return cur;
+}
+
+int grid_for(uint64_t n, int threads) {
+    uint64_t g = (n + threads - 1) / threads;
+    return (int)std::min<uint64_t>(std::max<uint64_t>(g, 1), (uint64_t)num_sms() * 16);
+}
+
+// Sort segment [S0, S0+len) of (out_keys, out_perm) by (key, index) with the radix area.
+template <typename KeyT, bool PERM>
+int radix_segment(KeyT* out_keys, uint32_t* out_perm, uint64_t S0, uint64_t len, bool input_ordered,
+                  void* ws, const Layout& L, cudaStream_t s, Launches& nl) {
+    using Bits = typename KeyTraits<KeyT>::Bits;
+    char* base = at<char>(ws, L.radix);
+    Bits* k0 = reinterpret_cast<Bits*>(base);
+    Bits* k1 = reinterpret_cast<Bits*>(base + align_up(len * sizeof(Bits)));
+    uint32_t* v0 = PERM ? reinterpret_cast<uint32_t*>(base + 2 * align_up(len * sizeof(Bits))) : nullptr;
+    uint32_t* v1 = PERM ? reinterpret_cast<uint32_t*>(base + 2 * align_up(len * sizeof(Bits)) + align_up(len * 4)) : nullptr;
+    uint32_t* gh = reinterpret_cast<uint32_t*>(base + 2 * align_up(len * sizeof(Bits)) + (PERM ? 2 * align_up(len * 4) : 0));
+    k_to_ord<KeyT><<<grid_for(len, 256), 256, 0, s>>>(out_keys + S0, k0, nullptr, len, 0);
+    if (PERM) CK(cudaMemcpyAsync(v0, out_perm + S0, len * 4, cudaMemcpyDeviceToDevice, s));
+    cudaError_t err;
+    int cur = radix_sort_pairs<Bits>(k0, v0, k1, v1, gh, len, PERM && !input_ordered, s, nl, err);
+    if (err != cudaSuccess) return MLSORT_ERR_CUDA;
+    k_from_ord<KeyT><<<grid_for(len, 256), 256, 0, s>>>(cur ? k1 : k0, out_keys + S0, len);
+    if (PERM) CK(cudaMemcpyAsync(out_perm + S0, cur ? v1 : v0, len * 4, cudaMemcpyDeviceToDevice, s));
+    nl.count += 2;
+    CK(cudaGetLastError());
+    return MLSORT_OK;
+}
+
+// Whole-input conventional sort (fallback): stable radix sort of (key, iota).
+template <typename KeyT, bool PERM>
+int fallback_sort(const KeyT* keys, uint64_t n, KeyT* out_keys, uint32_t* out_perm, void* ws, const Layout& L,
+                  cudaStream_t s, Launches& nl) {
+    using Bits = typename KeyTraits<KeyT>::Bits;
+    char* base = at<char>(ws, L.radix);
+    Bits* k0 = reinterpret_cast<Bits*>(base);
+    Bits* k1 = reinterpret_cast<Bits*>(base + align_up(n * sizeof(Bits)));
+    uint32_t* v0 = PERM ? reinterpret_cast<uint32_t*>(base + 2 * align_up(n * sizeof(Bits))) : nullptr;
+    uint32_t* v1 = PERM ? reinterpret_cast<uint32_t*>(base + 2 * align_up(n * sizeof(Bits)) + align_up(n * 4)) : nullptr;
+    uint32_t* gh = reinterpret_cast<uint32_t*>(base + 2 * align_up(n * sizeof(Bits)) + (PERM ? 2 * align_up(n * 4) : 0));
+    k_to_ord<KeyT><<<grid_for(n, 256), 256, 0, s>>>(keys, k0, v0, n, 0);
+    cudaError_t err;
+    int cur = radix_sort_pairs<Bits>(k0, v0, k1, v1, gh, n, false, s, nl, err);
+    if (err != cudaSuccess) return MLSORT_ERR_CUDA;
+    k_from_ord<KeyT><<<grid_for(n, 256), 256, 0, s>>>(cur ? k1 : k0, out_keys, n);
+    if (PERM) CK(cudaMemcpyAsync(out_perm, cur ? v1 : v0, n * 4, cudaMemcpyDeviceToDevice, s));
+    nl.count += 2;
+    CK(cudaGetLastError());
+    return MLSORT_OK;
+}
+
+K1Params k1_params(const Weights& w, const Plan& p, uint64_t B) {
+    K1Params kp;
+    kp.lo_d = w.lo;
+    kp.hi_d = w.hi;
+    kp.lo_f = (float)w.lo;
+    kp.bm.Bf = (float)B;
+    kp.bm.Bm1 = (uint32_t)(B - 1);
+    kp.fine_bits = p.fb;
+    kp.num_coarse = p.C;
+    kp.num_tiles = p.T;
+    kp.n = p.n;
+    return kp;
+}
+
+// The core pipeline shared by mlsort_sort (predict) and mlsort_sort_records (GIVEN buckets).
+template <typename KeyT, bool PERM, bool GIVEN>
+int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int pred, KeyT* out_keys,
+                 uint32_t* out_perm, void* ws, uint64_t ws_bytes, cudaStream_t s, mlsort_info* info,
+                 const uint32_t* bucket_in, const uint32_t* idx_in, uint32_t b_lo) {
+    Launches nl;
+    const Plan p = make_plan(n, B, sizeof(KeyT), PERM);
+    const Layout L = make_layout(p);
+    if (ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign)) return MLSORT_ERR_WORKSPACE;
+    DevStatus* dst = at<DevStatus>(ws, L.status);
+    {
+        DevStatus init;
+        std::memset(&init, 0, sizeof(init));
+        init.bad_index = ~0ull;
+        CK(cudaMemcpyAsync(dst, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaMemsetAsync(at<void>(ws, L.range_start), 0xff, (size_t)p.C * p.R * 8, s));
+
+    FoldedWeights fw;
+    uint32_t mpad = 16;
+    K1Params kp;
+    if (!GIVEN) {
+        mpad = mpad_of(w->m);
+        fw = fold(*w, mpad);
+        kp = k1_params(*w, p, B);
+    } else {
+        std::memset(&fw, 0, sizeof(fw));
+        Weights dummy;
+        dummy.lo = 0;
+        dummy.hi = 1;
+        kp = k1_params(dummy, p, B);
+        kp.lo_d = -INFINITY;
+        kp.hi_d = INFINITY;
+    }
+    if (pred != kPredMufu) pred = kPredMixed;
+    CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kp, ws, L, s, bucket_in, idx_in, b_lo)));
+    k2_coarse_starts<<<p.C + 1, kThreads, 0, s>>>(at<uint16_t>(ws, L.matrix), p.T, at<unsigned long long>(ws, L.starts));
+    CK(cudaGetLastError());
+    CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s)));
+    k4_big_gather<KeyT, PERM><<<num_sms(), kK3Threads, 0, s>>>(
+        p.T, p.R, at<KeyT>(ws, L.part_keys), at<uint16_t>(ws, L.part_fine),
+        PERM ? at<uint32_t>(ws, L.part_idx) : nullptr, at<uint16_t>(ws, L.matrix),
+        at<unsigned long long>(ws, L.starts), out_keys, out_perm, at<unsigned long long>(ws, L.range_start), dst,
+        at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.flags), &dst->ticket);
+    CK(cudaGetLastError());
+    const uint64_t nranges = (uint64_t)p.C * p.R;
+    k5_boundary_verify<KeyT, PERM><<<(unsigned)((nranges + 255) / 256), 256, 0, s>>>(
+        at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
+    CK(cudaGetLastError());
+    nl.count += 5;
+
+    DevStatus* hs = host_status();
+    CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    DevStatus st = *hs;
+    if (info) {
+        info->num_coarse = p.C;
+        info->tail_lo = st.tail_lo;
+        info->tail_hi = st.tail_hi;
+        info->max_coarse = st.max_coarse;
+        info->big_buckets = st.big_count;
+    }
+    if (st.bad_index != ~0ull) {
+        if (info) info->bad_index = (int64_t)st.bad_index;
+        return MLSORT_ERR_NONFINITE_KEY;
+    }
+    uint64_t violations = st.violations;
+    if (st.overflow > 0) {   // K4 radix for big buckets that are not all-equal
+        std::vector<uint32_t> big(st.big_count), flags(st.big_count);
+        std::vector<unsigned long long> starts(p.C + 1);
+        CK(cudaMemcpyAsync(big.data(), at<uint32_t>(ws, L.big_list), big.size() * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(flags.data(), at<uint32_t>(ws, L.flags), flags.size() * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(starts.data(), at<unsigned long long>(ws, L.starts), starts.size() * 8,
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (size_t k = 0; k < big.size(); ++k) {
+            const bool equal = flags[k] & 1u, ordered = flags[k] & 2u;
+            if (equal && (!PERM || ordered)) continue;
+            const uint64_t S0 = starts[big[k]], len = starts[big[k] + 1] - S0;
+            int rc = radix_segment<KeyT, PERM>(out_keys, out_perm, S0, len, ordered, ws, L, s, nl);
+            if (rc) return rc;
+        }
+        // re-verify every boundary now that all ranges are final
+        CK(cudaMemsetAsync(&dst->violations, 0, 8, s));
+        k5_boundary_verify<KeyT, PERM><<<(unsigned)((nranges + 255) / 256), 256, 0, s>>>(
+            at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
+        CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        violations = st.violations + hs->violations;
+    }
+    if (info) info->repairs = violations;
+    if (violations > 0) {   // reading A14: escalate to the conventional sort
+        if (GIVEN) {
+            // records path: sort (key, global index) pairs of the received records
+            using Bits = typename KeyTraits<KeyT>::Bits;
+            char* base = at<char>(ws, L.radix);
+            Bits* k0 = reinterpret_cast<Bits*>(base);
+            Bits* k1 = reinterpret_cast<Bits*>(base + align_up(n * sizeof(Bits)));
+            uint32_t* v0 = PERM ? reinterpret_cast<uint32_t*>(base + 2 * align_up(n * sizeof(Bits))) : nullptr;
+            uint32_t* v1 = PERM ? reinterpret_cast<uint32_t*>(base + 2 * align_up(n * sizeof(Bits)) + align_up(n * 4)) : nullptr;
+            uint32_t* gh = reinterpret_cast<uint32_t*>(base + 2 * align_up(n * sizeof(Bits)) + (PERM ? 2 * align_up(n * 4) : 0));
+            k_to_ord<KeyT><<<grid_for(n, 256), 256, 0, s>>>(keys, k0, nullptr, n, 0);
+            if (PERM) CK(cudaMemcpyAsync(v0, idx_in, n * 4, cudaMemcpyDeviceToDevice, s));
+            cudaError_t err;
+            int cur = radix_sort_pairs<Bits>(k0, v0, k1, v1, gh, n, PERM, s, nl, err);
+            if (err != cudaSuccess) return MLSORT_ERR_CUDA;
+            k_from_ord<KeyT><<<grid_for(n, 256), 256, 0, s>>>(cur ? k1 : k0, out_keys, n);
+            if (PERM) CK(cudaMemcpyAsync(out_perm, cur ? v1 : v0, n * 4, cudaMemcpyDeviceToDevice, s));
+        } else {
+            int rc = fallback_sort<KeyT, PERM>(keys, n, out_keys, out_perm, ws, L, s, nl);
+            if (rc) return rc;
+        }
+        CK(cudaStreamSynchronize(s));
+        if (info) info->fallback_used = 1;
+    }
+    if (info) info->kernel_launches = nl.count;
+    return MLSORT_OK;
+}
+
+uint64_t workspace_bytes(uint64_t n, mlsort_dtype dt, uint64_t B, bool perm) {
+    const Plan p = make_plan(n, B, dt == MLSORT_F32 ? 4 : 8, perm);
+    return make_layout(p).total;
+}
+
+}  // namespace
+
+// ==================================================================== C ABI
+
+extern "C" int mlsort_sort_workspace_size(uint64_t n, mlsort_dtype dt, const mlsort_opts* o, int want_perm,
+                                          uint64_t* bytes) {
+    if (!bytes || (dt != MLSORT_F32 && dt != MLSORT_F64)) return MLSORT_ERR_INVALID_ARG;
+    const uint64_t B = (o && o->num_buckets) ? o->num_buckets : n;
+    if (n == 0) {
+        *bytes = 0;
+        return MLSORT_OK;
+    }
+    if (B > (1ull << 30) || B < 1) return MLSORT_ERR_INVALID_ARG;
+    *bytes = workspace_bytes(n, dt, B, want_perm != 0) + 2 * kAlign;
+    return MLSORT_OK;
+}
+
+extern "C" int mlsort_sort(const void* d_keys, const uint32_t* d_payload, uint64_t n, mlsort_dtype dt,
+                           const mlsort_weights* wh, const mlsort_opts* o, void* d_out_keys, uint32_t* d_out_perm,
+                           uint32_t* d_out_payload, void* d_ws, uint64_t ws_bytes, void* stream, mlsort_info* info) {
+    if (info) {
+        std::memset(info, 0, sizeof(*info));
+        info->bad_index = -1;
+    }
+    if (dt != MLSORT_F32 && dt != MLSORT_F64) return MLSORT_ERR_INVALID_ARG;
+    if (n == 0) return MLSORT_OK;
+    if (!d_keys || !wh || !d_out_keys || d_keys == d_out_keys) return MLSORT_ERR_INVALID_ARG;
+    if (d_out_payload && (!d_payload || !d_out_perm)) return MLSORT_ERR_INVALID_ARG;
+    if (d_out_perm && n >= (1ull << 32)) return MLSORT_ERR_INVALID_ARG;
+    if (n >= (1ull << 32)) return MLSORT_ERR_INVALID_ARG;
+    if (o && (o->reserved[0] || o->reserved[1] || o->reserved[2] || o->reserved[3])) return MLSORT_ERR_INVALID_ARG;
+    const uint64_t B = (o && o->num_buckets) ? o->num_buckets : n;
+    if (B > (1ull << 30)) return MLSORT_ERR_INVALID_ARG;
+    const Weights* w = reinterpret_cast<const Weights*>(wh);
+    const int pred = (o && o->predictor == MLSORT_PRED_MUFU) ? kPredMufu : kPredMixed;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // align the workspace base
+    uintptr_t wsp = reinterpret_cast<uintptr_t>(d_ws);
+    uintptr_t aligned = (wsp + kAlign - 1) / kAlign * kAlign;
+    if (!d_ws || ws_bytes < (aligned - wsp)) return MLSORT_ERR_WORKSPACE;
+    void* ws = reinterpret_cast<void*>(aligned);
+    ws_bytes -= (aligned - wsp);
+    const bool perm = d_out_perm != nullptr;
+    int rc;
+    if (dt == MLSORT_F32) {
+        rc = perm ? run_pipeline<float, true, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, d_out_perm,
+                                                     ws, ws_bytes, s, info, nullptr, nullptr, 0)
+                  : run_pipeline<float, false, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, nullptr,
+                                                      ws, ws_bytes, s, info, nullptr, nullptr, 0);
+    } else {
+        rc = perm ? run_pipeline<double, true, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
+                                                      d_out_perm, ws, ws_bytes, s, info, nullptr, nullptr, 0)
+                  : run_pipeline<double, false, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
+                                                       nullptr, ws, ws_bytes, s, info, nullptr, nullptr, 0);
+    }
+    if (rc == MLSORT_OK && d_out_payload) {
+        k_gather_payload<float><<<grid_for(n, 256), 256, 0, s>>>(d_out_perm, d_payload, d_out_payload, n);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
+        if (info) info->kernel_launches += 1;
+    }
+    return rc;
+}
+
+extern "C" int mlsort_sort_host_workspace_size(uint64_t n, mlsort_dtype dt, const mlsort_opts* o, int want_perm,
+                                               uint64_t* bytes) {
+    uint64_t b = 0;
+    int rc = mlsort_sort_workspace_size(n, dt, o, want_perm, &b);
+    if (rc) return rc;
+    const size_t ks = dt == MLSORT_F32 ? 4 : 8;
+    *bytes = b + 2 * align_up(n * ks) + (want_perm ? align_up(n * 4) : 0) + kAlign;
+    return MLSORT_OK;
+}
+
+extern "C" int mlsort_sort_host(const void* h_keys, uint64_t n, mlsort_dtype dt, const mlsort_weights* w,
+                                const mlsort_opts* o, void* h_out_keys, uint32_t* h_out_perm, void* d_ws,
+                                uint64_t ws_bytes, void* stream, mlsort_info* info) {
+    if (dt != MLSORT_F32 && dt != MLSORT_F64) return MLSORT_ERR_INVALID_ARG;
+    if (n == 0) {
+        if (info) {
+            std::memset(info, 0, sizeof(*info));
+            info->bad_index = -1;
+        }
+        return MLSORT_OK;
+    }
+    if (!h_keys || !h_out_keys || !d_ws) return MLSORT_ERR_INVALID_ARG;
+    const size_t ks = dt == MLSORT_F32 ? 4 : 8;
+    uintptr_t wsp = reinterpret_cast<uintptr_t>(d_ws);
+    uintptr_t aligned = (wsp + kAlign - 1) / kAlign * kAlign;
+    const uint64_t need_io = 2 * align_up(n * ks) + (h_out_perm ? align_up(n * 4) : 0);
+    if (ws_bytes < (aligned - wsp) + need_io) return MLSORT_ERR_WORKSPACE;
+    char* base = reinterpret_cast<char*>(aligned);
+    void* d_in = base;
+    void* d_out = base + align_up(n * ks);
+    uint32_t* d_perm = h_out_perm ? reinterpret_cast<uint32_t*>(base + 2 * align_up(n * ks)) : nullptr;
+    void* rest = base + need_io;
+    const uint64_t rest_bytes = ws_bytes - (aligned - wsp) - need_io;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaMemcpyAsync(d_in, h_keys, n * ks, cudaMemcpyHostToDevice, s));
+    int rc = mlsort_sort(d_in, nullptr, n, dt, w, o, d_out, d_perm, nullptr, rest, rest_bytes, stream, info);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h_out_keys, d_out, n * ks, cudaMemcpyDeviceToHost, s));
+    if (h_out_perm) CK(cudaMemcpyAsync(h_out_perm, d_perm, n * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return MLSORT_OK;
+}
+
+// ---------------------------------------------------------------- approximate ranking
+namespace {
+template <typename KeyT, int MPAD, int PRED>
+__global__ void __launch_bounds__(256)
+k_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Params p, float* __restrict__ y_out,
+          uint32_t* __restrict__ b_out) {
+    constexpr int G = 8;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * G) {
+        float u[G], y[G];
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            const uint64_t i = i0 + (uint64_t)q * stride;
+            KeyT x = i < n ? keys[i] : (KeyT)p.lo_d;
+            if (!KeyTraits<KeyT>::finite(x)) x = (KeyT)p.lo_d;
+            u[q] = key_to_u<KeyT>(x, p);
+        }
+        gvm_forward_f32<MPAD, PRED, G>(fw, u, y);
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            const uint64_t i = i0 + (uint64_t)q * stride;
+            if (i < n) {
+                if (y_out) y_out[i] = y[q];
+                if (b_out) b_out[i] = bucket_of(y[q], p.bm);
+            }
+        }
+    }
+}
+
+template <typename KeyT>
+int launch_predict(const KeyT* keys, uint64_t n, const Weights& w, uint64_t B, int pred, float* y, uint32_t* b,
+                   cudaStream_t s) {
+    const uint32_t mpad = mpad_of(w.m);
+    FoldedWeights fw = fold(w, mpad);
+    Plan p;
+    p.n = n;
+    K1Params kp = k1_params(w, p, B);
+    const int grid = num_sms() * 8;
+#define PCASE(M)                                                                                    \
+    if (mpad == M) {                                                                                \
+        if (pred == kPredMufu) k_predict<KeyT, M, kPredMufu><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b); \
+        else k_predict<KeyT, M, kPredMixed><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b);            \
+    }
+    PCASE(16) PCASE(32) PCASE(64)
+#undef PCASE
+    CK(cudaGetLastError());
+    return MLSORT_OK;
+}
+}  // namespace
+
+extern "C" int mlsort_predict(const void* d_keys, uint64_t n, mlsort_dtype dt, const mlsort_weights* wh,
+                              uint64_t num_buckets, int32_t predictor, float* d_y, uint32_t* d_bucket, void* stream) {
+    if (dt != MLSORT_F32 && dt != MLSORT_F64) return MLSORT_ERR_INVALID_ARG;
+    if (n == 0) return MLSORT_OK;
+    if (!d_keys || !wh) return MLSORT_ERR_INVALID_ARG;
+    const uint64_t B = num_buckets ? num_buckets : n;
+    if (B > (1ull << 32)) return MLSORT_ERR_INVALID_ARG;
+    const Weights* w = reinterpret_cast<const Weights*>(wh);
+    const int pred = predictor == MLSORT_PRED_MUFU ? kPredMufu : kPredMixed;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return dt == MLSORT_F32 ? launch_predict<float>((const float*)d_keys, n, *w, B, pred, d_y, d_bucket, s)
+                            : launch_predict<double>((const double*)d_keys, n, *w, B, pred, d_y, d_bucket, s);
+}
+
+// ---------------------------------------------------------------- multi-GPU building blocks
+extern "C" int mlsort_dist_partition_workspace_size(uint64_t n_local, mlsort_dtype dt, uint32_t nranks,
+                                                    uint64_t* bytes) {
+    if (!bytes || nranks < 1 || nranks > kMaxRanks || (dt != MLSORT_F32 && dt != MLSORT_F64)) return MLSORT_ERR_INVALID_ARG;
+    const uint64_t nchunks = (n_local + kRadixChunk - 1) / kRadixChunk;
+    *bytes = align_up(sizeof(DevStatus)) + align_up(n_local * 4) + align_up(nchunks * kMaxRanks * 4) + 2 * kAlign;
+    return MLSORT_OK;
+}
+
+extern "C" int mlsort_dist_partition(const void* d_shard, uint64_t n_local, uint64_t global_offset, uint64_t n_global,
+                                     mlsort_dtype dt, const mlsort_weights* wh, const mlsort_opts* o, uint32_t nranks,
+                                     void* d_rec_keys, uint32_t* d_rec_bucket, uint32_t* d_rec_index,
+                                     uint64_t* h_send_counts, void* d_ws, uint64_t ws_bytes, void* stream,
+                                     mlsort_info* info) {
+    if (info) {
+        std::memset(info, 0, sizeof(*info));
+        info->bad_index = -1;
+    }
+    if (dt != MLSORT_F32 && dt != MLSORT_F64) return MLSORT_ERR_INVALID_ARG;
+    if (!wh || !h_send_counts || nranks < 1 || nranks > kMaxRanks) return MLSORT_ERR_INVALID_ARG;
+    if (n_global >= (1ull << 32) || global_offset + n_local > n_global) return MLSORT_ERR_INVALID_ARG;
+    for (uint32_t g = 0; g < nranks; ++g) h_send_counts[g] = 0;
+    if (n_local == 0) return MLSORT_OK;
+    if (!d_shard || !d_rec_keys || !d_rec_bucket) return MLSORT_ERR_INVALID_ARG;
+    const uint64_t B = (o && o->num_buckets) ? o->num_buckets : n_global;
+    if (B > (1ull << 30)) return MLSORT_ERR_INVALID_ARG;
+    const Weights* w = reinterpret_cast<const Weights*>(wh);
+    const int pred = (o && o->predictor == MLSORT_PRED_MUFU) ? kPredMufu : kPredMixed;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uintptr_t wsp = reinterpret_cast<uintptr_t>(d_ws);
+    uintptr_t aligned = (wsp + kAlign - 1) / kAlign * kAlign;
+    uint64_t need = 0;
+    mlsort_dist_partition_workspace_size(n_local, dt, nranks, &need);
+    if (!d_ws || ws_bytes < need) return MLSORT_ERR_WORKSPACE;
+    char* base = reinterpret_cast<char*>(aligned);
+    DevStatus* dst = reinterpret_cast<DevStatus*>(base);
+    uint32_t* bucket_tmp = reinterpret_cast<uint32_t*>(base + align_up(sizeof(DevStatus)));
+    uint32_t* ghist = reinterpret_cast<uint32_t*>(base + align_up(sizeof(DevStatus)) + align_up(n_local * 4));
+    DevStatus init;
+    std::memset(&init, 0, sizeof(init));
+    init.bad_index = ~0ull;
+    CK(cudaMemcpyAsync(dst, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+    const uint32_t mpad = mpad_of(w->m);
+    FoldedWeights fw = fold(*w, mpad);
+    Plan p;
+    p.n = n_local;
+    K1Params kp = k1_params(*w, p, B);
+    int rc = dt == MLSORT_F32
+                 ? dist_partition<float>((const float*)d_shard, n_local, global_offset, B, nranks, mpad, pred, fw, kp,
+                                         (float*)d_rec_keys, d_rec_bucket, d_rec_index, bucket_tmp, ghist, dst,
+                                         h_send_counts, s)
+                 : dist_partition<double>((const double*)d_shard, n_local, global_offset, B, nranks, mpad, pred, fw,
+                                          kp, (double*)d_rec_keys, d_rec_bucket, d_rec_index, bucket_tmp, ghist, dst,
+                                          h_send_counts, s);
+    if (rc) return rc;
+    DevStatus* hs = host_status();
+    CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (info) {
+        info->tail_lo = hs->tail_lo;
+        info->tail_hi = hs->tail_hi;
+        info->kernel_launches = 3;
+    }
+    if (hs->bad_index != ~0ull) {
+        if (info) info->bad_index = (int64_t)hs->bad_index;
+        return MLSORT_ERR_NONFINITE_KEY;
+    }
+    return MLSORT_OK;
+}
+
+extern "C" int mlsort_sort_records_workspace_size(uint64_t n, mlsort_dtype dt, uint64_t bucket_lo, uint64_t bucket_hi,
+                                                  uint64_t* bytes) {
+    if (!bytes || bucket_hi <= bucket_lo) return MLSORT_ERR_INVALID_ARG;
+    mlsort_opts o;
+    std::memset(&o, 0, sizeof(o));
+    o.num_buckets = bucket_hi - bucket_lo;
+    if (n == 0) {
+        *bytes = 0;
+        return MLSORT_OK;
+    }
+    return mlsort_sort_workspace_size(n, dt, &o, 1, bytes);
+}
+
+extern "C" int mlsort_sort_records(const void* d_keys, const uint32_t* d_bucket, const uint32_t* d_index, uint64_t n,
+                                   mlsort_dtype dt, uint64_t bucket_lo, uint64_t bucket_hi, void* d_out_keys,
+                                   uint32_t* d_out_index, void* d_ws, uint64_t ws_bytes, void* stream,
+                                   mlsort_info* info) {
+    if (info) {
+        std::memset(info, 0, sizeof(*info));
+        info->bad_index = -1;
+    }
+    if (dt != MLSORT_F32 && dt != MLSORT_F64) return MLSORT_ERR_INVALID_ARG;
+    if (n == 0) return MLSORT_OK;
+    if (!d_keys || !d_bucket || !d_out_keys || bucket_hi <= bucket_lo) return MLSORT_ERR_INVALID_ARG;
+    if ((d_index == nullptr) != (d_out_index == nullptr)) return MLSORT_ERR_INVALID_ARG;
+    if (n >= (1ull << 32) || bucket_hi - bucket_lo > (1ull << 30)) return MLSORT_ERR_INVALID_ARG;
+    uintptr_t wsp = reinterpret_cast<uintptr_t>(d_ws);
+    uintptr_t aligned = (wsp + kAlign - 1) / kAlign * kAlign;
+    if (!d_ws || ws_bytes < (aligned - wsp)) return MLSORT_ERR_WORKSPACE;
+    void* ws = reinterpret_cast<void*>(aligned);
+    ws_bytes -= (aligned - wsp);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t B = bucket_hi - bucket_lo;
+    const uint32_t blo = (uint32_t)bucket_lo;
+    if (dt == MLSORT_F32)
+        return d_index ? run_pipeline<float, true, true>((const float*)d_keys, n, B, nullptr, kPredMixed,
+                                                         (float*)d_out_keys, d_out_index, ws, ws_bytes, s, info,
+                                                         d_bucket, d_index, blo)
+                       : run_pipeline<float, false, true>((const float*)d_keys, n, B, nullptr, kPredMixed,
+                                                          (float*)d_out_keys, nullptr, ws, ws_bytes, s, info,
+                                                          d_bucket, nullptr, blo);
+    return d_index ? run_pipeline<double, true, true>((const double*)d_keys, n, B, nullptr, kPredMixed,
+                                                      (double*)d_out_keys, d_out_index, ws, ws_bytes, s, info,
+                                                      d_bucket, d_index, blo)
+                   : run_pipeline<double, false, true>((const double*)d_keys, n, B, nullptr, kPredMixed,
+                                                       (double*)d_out_keys, nullptr, ws, ws_bytes, s, info, d_bucket,
+                                                       nullptr, blo);
+}
