@@ -38,7 +38,7 @@ template <> __device__ __forceinline__ float key_to_u<double>(double x, const K1
     return (float)(x - p.lo_d);
 }
 
-// Dynamic shared memory: hist[C] u32 | stage_key[kTile] KeyT | stage_idx[kTile] u32 (PERM)
+// Dynamic shared memory: stage_key[kTile] KeyT | stage_idx[kTile] u32 (PERM) | hist[C] u32
 //                        | stage_fine[kTile] u16 | scratch.
 template <typename KeyT, bool PERM>
 __host__ __device__ constexpr size_t k1_smem_bytes(uint32_t num_coarse) {
@@ -58,13 +58,12 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
                      const uint32_t* __restrict__ idx_in = nullptr, uint32_t b_lo = 0) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t C = p.num_coarse;
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
-    KeyT* stage_key = reinterpret_cast<KeyT*>(smem + (size_t)C * 4);
-    uint32_t* stage_idx = reinterpret_cast<uint32_t*>(smem + (size_t)C * 4 + (size_t)kTile * sizeof(KeyT));
-    uint16_t* stage_fine = reinterpret_cast<uint16_t*>(smem + (size_t)C * 4 + (size_t)kTile * sizeof(KeyT) +
-                                                       (PERM ? (size_t)kTile * 4 : 0));
-    uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + (size_t)C * 4 + (size_t)kTile * sizeof(KeyT) +
-                                                    (PERM ? (size_t)kTile * 4 : 0) + (size_t)kTile * 2);
+    // layout: stage_key[kTile] KeyT | stage_idx[kTile] u32 (PERM) | hist[C] u32 | stage_fine[kTile] u16 | scratch
+    KeyT* stage_key = reinterpret_cast<KeyT*>(smem);
+    uint32_t* stage_idx = reinterpret_cast<uint32_t*>(smem + (size_t)kTile * sizeof(KeyT));
+    uint32_t* hist = stage_idx + (PERM ? kTile : 0);
+    uint16_t* stage_fine = reinterpret_cast<uint16_t*>(hist + C);
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(stage_fine + kTile);
 
     const int tid = threadIdx.x;
     const uint32_t tile = blockIdx.x;

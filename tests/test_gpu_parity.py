@@ -106,7 +106,14 @@ def test_sort_nonmonotone_weights(mls):
     w = mls.Weights.from_dict(pw)
     assert not w.check_monotone()
     info, _ = check_sort(mls, keys, w, w.params(), perm=True)
+    assert info["fallback_used"] == 1 or info["big_buckets"] > 0 or info["repairs"] > 0
+    # a decreasing model (w1 < 0, Eq. 4 violated for every neuron) inverts the bucket order:
+    # the verify pass must catch it and the conventional-sort fallback must repair it
+    w = mls.Weights.create(3, [-1, -1, -1], [0.3, 0.3, 0.4], [-0.5, 0, 0.5], [4, 4, 4], -3.0, 3.0)
+    info, _ = check_sort(mls, keys, w, w.params(), perm=True)
     assert info["fallback_used"] == 1 and info["repairs"] > 0
+    info, _ = check_sort(mls, keys, w, w.params(), perm=False)
+    assert info["fallback_used"] == 1
 
 
 def test_sort_half_out_of_range(mls):
