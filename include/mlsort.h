@@ -68,7 +68,9 @@ typedef struct {
     uint64_t num_buckets;   /* B, the number of rank buckets; 0 means B = n          */
     int32_t  predictor;     /* mlsort_predictor                                             */
     int32_t  verify;        /* 1 (default) = run the final boundary verify/repair pass      */
-    int32_t  reserved[4];   /* must be zero                                                 */
+    int32_t  timing;        /* 1 = record CUDA events around each kernel phase and report
+                               the device times in mlsort_info.phase_ms (bench/profiling)     */
+    int32_t  reserved[3];   /* must be zero                                                 */
 } mlsort_opts;
 
 typedef struct {
@@ -81,6 +83,8 @@ typedef struct {
     uint64_t max_coarse;    /* largest coarse bucket                                        */
     uint64_t big_buckets;   /* coarse buckets that took the overflow path                   */
     uint64_t kernel_launches; /* device kernels launched by this call                      */
+    float    phase_ms[6];   /* with opts->timing: K1 predict+partition, K2 coarse starts,
+                               K3 cluster sort, K4 overflow gather, K5 verify, whole call     */
 } mlsort_info;
 
 /* Monte-Carlo trainer configuration (S:104-S:107, S:170-S:172; every value is a repo

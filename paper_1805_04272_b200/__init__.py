@@ -46,16 +46,19 @@ class NonFiniteKeyError(MLSortError, ValueError):
 
 class _Opts(C.Structure):
     _fields_ = [("num_buckets", C.c_uint64), ("predictor", C.c_int32), ("verify", C.c_int32),
-                ("reserved", C.c_int32 * 4)]
+                ("timing", C.c_int32), ("reserved", C.c_int32 * 3)]
 
 
 class Info(C.Structure):
     _fields_ = [("bad_index", C.c_int64), ("repairs", C.c_uint64), ("fallback_used", C.c_int32),
                 ("num_coarse", C.c_uint32), ("tail_lo", C.c_uint64), ("tail_hi", C.c_uint64),
-                ("max_coarse", C.c_uint64), ("big_buckets", C.c_uint64), ("kernel_launches", C.c_uint64)]
+                ("max_coarse", C.c_uint64), ("big_buckets", C.c_uint64), ("kernel_launches", C.c_uint64),
+                ("phase_ms", C.c_float * 6)]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["phase_ms"] = list(self.phase_ms)
+        return d
 
 
 class _TrainCfg(C.Structure):
@@ -216,11 +219,12 @@ def _stream_ptr(stream):
     return C.c_void_p(stream.cuda_stream)
 
 
-def _opts(num_buckets: int, predictor: int) -> _Opts:
+def _opts(num_buckets: int, predictor: int, timing: bool = False) -> _Opts:
     o = _Opts()
     o.num_buckets = num_buckets
     o.predictor = predictor
     o.verify = 1
+    o.timing = 1 if timing else 0
     return o
 
 
@@ -237,12 +241,13 @@ class Sorter:
     loop) do not re-allocate."""
 
     def __init__(self, n: int, dtype, perm: bool, num_buckets: int = 0, predictor: int = PRED_DEFAULT,
-                 device=None):
+                 device=None, timing: bool = False):
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1805_04272_b200 requires a CUDA device (sm_100a); there is no CPU path")
         self.device = torch.device(device or "cuda")
         self.n, self.perm, self.num_buckets, self.predictor = n, perm, num_buckets, predictor
+        self.timing = timing
         self.dt = F32 if dtype in (np.float32, torch.float32, "f32") else F64
         self.ws_bytes = workspace_size(n, self.dt, perm, num_buckets, predictor)
         self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=self.device)
@@ -261,7 +266,7 @@ class Sorter:
             out_perm = torch.empty(n, dtype=torch.int32, device=keys.device)
         if payload is not None and out_payload is None:
             out_payload = torch.empty(n, dtype=torch.int32, device=keys.device)
-        o = _opts(self.num_buckets, self.predictor)
+        o = _opts(self.num_buckets, self.predictor, self.timing)
         info = Info()
         rc = lib().mlsort_sort(C.c_void_p(keys.data_ptr()),
                                C.c_void_p(payload.data_ptr()) if payload is not None else None, n, self.dt,

@@ -81,11 +81,13 @@ extern "C" int mlsort_fit(const void* h_sample, uint64_t n0, mlsort_dtype dtype,
     const double lo = a.front(), hi = a.back();
     if (!(lo < hi)) return MLSORT_ERR_TRAIN;                  // S:134 degenerate range
 
-    // Pairs (a'_i, i/N0), i = 0..N0-1, evenly subsampled by rank.
+    // Pairs (a'_i, i/N0), i = 0..N0-1, evenly subsampled by rank; the first and the
+    // last rank are always kept.
     uint64_t P = (cfg.max_pairs && cfg.max_pairs < n0) ? cfg.max_pairs : n0;
+    if (P < 2) P = n0;
     std::vector<double> xh(P), tgt(P);
     for (uint64_t k = 0; k < P; ++k) {
-        uint64_t i = (P == n0) ? k : (uint64_t)((double)k * (double)n0 / (double)P);
+        uint64_t i = (P == n0) ? k : (uint64_t)((double)k * (double)(n0 - 1) / (double)(P - 1));
         xh[k] = 2.0 * (a[i] - lo) / (hi - lo) - 1.0;
         tgt[k] = (double)i / (double)n0;
     }
@@ -127,6 +129,11 @@ extern "C" int mlsort_fit(const void* h_sample, uint64_t n0, mlsort_dtype dtype,
     rebuild();
     double loss = mse();
 
+    // Range constraint (repo decision): the fitted CDF may not exceed
+    // 1 - 1/(2 N0) at the largest sample key.  Without it the MSE optimum overshoots 1 near
+    // the top and every key above that point collapses into the clamped last bucket
+    // ("r_j would fall out of the range [0, N]").
+    const double y_top_max = 1.0 - 0.5 / (double)n0;
     Rng rng(cfg.seed);
     uint64_t accepts = 0;
     for (uint64_t it = 0; it < cfg.iterations && loss > cfg.target_loss; ++it) {
@@ -147,6 +154,7 @@ extern "C" int mlsort_fit(const void* h_sample, uint64_t n0, mlsort_dtype dtype,
         double s = 0;
         for (uint64_t k = 0; k < P; ++k) { double e = Y[k] - old[k] + col[k] - tgt[k]; s += e * e; }
         double nl = s / (double)P;
+        if (Y[P - 1] - old[P - 1] + col[P - 1] > y_top_max && nl < loss) continue;
         if (nl < loss) {                                                   // S:133 strict decrease
             for (uint64_t k = 0; k < P; ++k) Y[k] += col[k] - old[k];
             std::copy(col.begin(), col.end(), T.begin() + (size_t)j * P);

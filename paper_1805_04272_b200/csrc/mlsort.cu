@@ -373,11 +373,43 @@ K1Params k1_params(const Weights& w, const Plan& p, uint64_t B) {
 }
 
 // The core pipeline shared by mlsort_sort (predict) and mlsort_sort_records (GIVEN buckets).
+struct PhaseTimer {
+    bool on = false;
+    cudaEvent_t ev[6] = {};
+    int n = 0;
+    cudaStream_t s = nullptr;
+    void start(bool enable, cudaStream_t st) {
+        on = enable;
+        s = st;
+        if (!on) return;
+        for (auto& e : ev) cudaEventCreate(&e);
+        cudaEventRecord(ev[0], s);
+        n = 1;
+    }
+    void mark() {
+        if (on && n < 6) cudaEventRecord(ev[n++], s);
+    }
+    void finish(mlsort_info* info) {   // after the stream was synchronised
+        if (!on) return;
+        if (info) {
+            for (int i = 1; i < n; ++i) cudaEventElapsedTime(&info->phase_ms[i - 1], ev[i - 1], ev[i]);
+            cudaEventElapsedTime(&info->phase_ms[5], ev[0], ev[n - 1]);
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        on = false;
+    }
+    ~PhaseTimer() {
+        if (on)
+            for (auto& e : ev) cudaEventDestroy(e);
+    }
+};
+
 template <typename KeyT, bool PERM, bool GIVEN>
 int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int pred, KeyT* out_keys,
                  uint32_t* out_perm, void* ws, uint64_t ws_bytes, cudaStream_t s, mlsort_info* info,
-                 const uint32_t* bucket_in, const uint32_t* idx_in, uint32_t b_lo) {
+                 const uint32_t* bucket_in, const uint32_t* idx_in, uint32_t b_lo, bool timing = false) {
     Launches nl;
+    PhaseTimer tm;
     const Plan p = make_plan(n, B, sizeof(KeyT), PERM);
     const Layout L = make_layout(p);
     if (ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign)) return MLSORT_ERR_WORKSPACE;
@@ -407,25 +439,32 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         kp.hi_d = INFINITY;
     }
     if (pred != kPredMufu) pred = kPredMixed;
+    tm.start(timing, s);
     CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kp, ws, L, s, bucket_in, idx_in, b_lo)));
+    tm.mark();
     k2_coarse_starts<<<p.C + 1, kThreads, 0, s>>>(at<uint16_t>(ws, L.matrix), p.T, at<unsigned long long>(ws, L.starts));
     CK(cudaGetLastError());
+    tm.mark();
     CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s)));
+    tm.mark();
     k4_big_gather<KeyT, PERM><<<num_sms(), kK3Threads, 0, s>>>(
         p.T, p.R, at<KeyT>(ws, L.part_keys), at<uint16_t>(ws, L.part_fine),
         PERM ? at<uint32_t>(ws, L.part_idx) : nullptr, at<uint16_t>(ws, L.matrix),
         at<unsigned long long>(ws, L.starts), out_keys, out_perm, at<unsigned long long>(ws, L.range_start), dst,
         at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.flags), &dst->ticket);
     CK(cudaGetLastError());
+    tm.mark();
     const uint64_t nranges = (uint64_t)p.C * p.R;
     k5_boundary_verify<KeyT, PERM><<<(unsigned)((nranges + 255) / 256), 256, 0, s>>>(
         at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
     CK(cudaGetLastError());
+    tm.mark();
     nl.count += 5;
 
     DevStatus* hs = host_status();
     CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    tm.finish(info);
     DevStatus st = *hs;
     if (info) {
         info->num_coarse = p.C;
@@ -526,7 +565,7 @@ extern "C" int mlsort_sort(const void* d_keys, const uint32_t* d_payload, uint64
     if (d_out_payload && (!d_payload || !d_out_perm)) return MLSORT_ERR_INVALID_ARG;
     if (d_out_perm && n >= (1ull << 32)) return MLSORT_ERR_INVALID_ARG;
     if (n >= (1ull << 32)) return MLSORT_ERR_INVALID_ARG;
-    if (o && (o->reserved[0] || o->reserved[1] || o->reserved[2] || o->reserved[3])) return MLSORT_ERR_INVALID_ARG;
+    if (o && (o->reserved[0] || o->reserved[1] || o->reserved[2])) return MLSORT_ERR_INVALID_ARG;
     const uint64_t B = (o && o->num_buckets) ? o->num_buckets : n;
     if (B > (1ull << 30)) return MLSORT_ERR_INVALID_ARG;
     const Weights* w = reinterpret_cast<const Weights*>(wh);
@@ -539,17 +578,18 @@ extern "C" int mlsort_sort(const void* d_keys, const uint32_t* d_payload, uint64
     void* ws = reinterpret_cast<void*>(aligned);
     ws_bytes -= (aligned - wsp);
     const bool perm = d_out_perm != nullptr;
+    const bool timing = o && o->timing;
     int rc;
     if (dt == MLSORT_F32) {
         rc = perm ? run_pipeline<float, true, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, d_out_perm,
-                                                     ws, ws_bytes, s, info, nullptr, nullptr, 0)
+                                                     ws, ws_bytes, s, info, nullptr, nullptr, 0, timing)
                   : run_pipeline<float, false, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, nullptr,
-                                                      ws, ws_bytes, s, info, nullptr, nullptr, 0);
+                                                      ws, ws_bytes, s, info, nullptr, nullptr, 0, timing);
     } else {
         rc = perm ? run_pipeline<double, true, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
-                                                      d_out_perm, ws, ws_bytes, s, info, nullptr, nullptr, 0)
+                                                      d_out_perm, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing)
                   : run_pipeline<double, false, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
-                                                       nullptr, ws, ws_bytes, s, info, nullptr, nullptr, 0);
+                                                       nullptr, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing);
     }
     if (rc == MLSORT_OK && d_out_payload) {
         k_gather_payload<float><<<grid_for(n, 256), 256, 0, s>>>(d_out_perm, d_payload, d_out_payload, n);
