@@ -18,9 +18,10 @@ struct DevStatus {
     unsigned long long big_count;   // coarse buckets routed to the overflow path
     unsigned long long big_elems;   // elements in those buckets
     unsigned long long max_coarse;  // largest coarse bucket
-    unsigned long long overflow;    // internal capacity overflow (must be 0)
-    unsigned long long ticket;      // dynamic CTA ticket for the ordered K3 look-back
-    unsigned long long pad[7];
+    unsigned long long overflow;    // big buckets that still need the K4 radix pass
+    unsigned long long ticket;      // dynamic CTA ticket (K4 persistent loop)
+    unsigned long long region_overflow;   // K1 pieces that did not fit their coarse region
+    unsigned long long pad[6];
 };
 
 // ---- IEEE-754 totalOrder as unsigned integers (reading A10): negative -> ~bits,

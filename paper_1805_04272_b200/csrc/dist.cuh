@@ -33,7 +33,8 @@ k_dist_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Pa
     constexpr int G8 = 8;
 #pragma unroll 1
     for (int g = 0; g < kRadixItems / G8; ++g) {
-        float u[G8], y[G8];
+        float u[G8], ul[G8];
+        int32_t y[G8];
 #pragma unroll
         for (int q = 0; q < G8; ++q) {
             const uint64_t e = base + tid + (uint64_t)kRadixThreads * (g * G8 + q);
@@ -46,14 +47,14 @@ k_dist_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Pa
                 tl += (double)x < p.lo_d;
                 th += (double)x > p.hi_d;
             }
-            u[q] = key_to_u<KeyT>(x, p);
+            key_to_u<KeyT>(x, p, u[q], ul[q]);
         }
-        gvm_forward_f32<MPAD, PRED, G8>(fw, u, y);
+        gvm_forward_fxp<MPAD, PRED, G8, sizeof(KeyT) == 8>(fw, u, ul, y);
 #pragma unroll
         for (int q = 0; q < G8; ++q) {
             const uint64_t e = base + tid + (uint64_t)kRadixThreads * (g * G8 + q);
             if (e < n) {
-                const uint32_t b = bucket_of(y[q], p.bm);
+                const uint32_t b = bucket_of_fxp(y[q], p.bm);
                 bucket_out[e] = b;
                 atomicAdd(&h[owner_of(b, B, G)], 1u);
             }

@@ -4,11 +4,13 @@
 // each number is independent of each other", l.94).  Per key: u = x - lo; the GVM forward
 // pass (Eq. 3) on the SFU/FMA pipes; the rank bucket b = round(y*B) (l.65); the coarse id
 // c = b >> fine_bits.  Per tile: a shared-memory histogram over the C coarse ids, a block
-// scan, an shared-memory scatter that partitions the tile by c, and one coalesced store
-// of the partitioned tile (keys, fine bits b & (2^fine_bits - 1), and the input index for
-// stable/perm sorts).  The tile's exclusive coarse offsets go to a column-major matrix
-// M[c][t] (uint16) so that K3 can find coarse bucket c's piece in every tile; the column
-// sums of M are the global coarse-bucket starts.
+// scan, a shared-memory scatter that partitions the tile by c, one global atomicAdd per
+// non-empty coarse bucket that reserves the tile's piece in that bucket's region (regions
+// are sized at kRegionFactor x the average bucket), and a store of every piece straight
+// into its region (keys, fine bits b & (2^fine_bits - 1), and the input index for perm
+// sorts).  K3 then reads each coarse bucket contiguously.  The
+// per-bucket cursors end as the exact bucket sizes; an overfull region sets the overflow
+// flag and the call falls back to the conventional sort.
 #pragma once
 
 #include "common.cuh"
@@ -16,55 +18,62 @@
 
 namespace mlsort {
 
-constexpr int kTile = 8192;                   // keys per K1 tile
-constexpr int kKeysPerThread = kTile / kThreads;   // 16
+constexpr int kTileSmall = 8192;              // keys per K1 tile (stable/perm sorts)
+constexpr int kTileLarge = 16384;             // keys per K1 tile (key-only sorts)
 constexpr int kGroup = 8;                      // keys evaluated together (ILP)
 
 struct K1Params {
-    double lo_d, hi_d;       // input_lo / input_hi of the weights (tail diagnostic, f64 u)
-    float lo_f;              // input_lo rounded to f32 (f32 u = x - lo_f)
+    double lo_d, hi_d;       // input_lo / input_hi of the weights (tail diagnostic)
+    double x0_d;             // origin of u = x - x0 (f64 keys)
+    float x0_f;              // origin of u = x - x0 (f32 keys; 0 or input_lo rounded)
+    float lo_tf, hi_tf;      // f32 keys: x < lo_d <=> x < lo_tf, x > hi_d <=> x > hi_tf
     BucketMap bm;
     uint32_t fine_bits;      // b = c * 2^fine_bits + fine
     uint32_t num_coarse;     // C
     uint32_t num_tiles;      // T
+    uint32_t capc;           // region capacity (elements) of every coarse bucket
     uint64_t n;
 };
 
-template <typename KeyT> __device__ __forceinline__ float key_to_u(KeyT x, const K1Params& p);
-template <> __device__ __forceinline__ float key_to_u<float>(float x, const K1Params& p) {
-    return x - p.lo_f;
+template <typename KeyT> __device__ __forceinline__ void key_to_u(KeyT x, const K1Params& p, float& uh, float& ul);
+template <> __device__ __forceinline__ void key_to_u<float>(float x, const K1Params& p, float& uh, float& ul) {
+    uh = x - p.x0_f;
+    ul = 0.0f;
 }
-template <> __device__ __forceinline__ float key_to_u<double>(double x, const K1Params& p) {
-    return (float)(x - p.lo_d);
+template <> __device__ __forceinline__ void key_to_u<double>(double x, const K1Params& p, float& uh, float& ul) {
+    const double u = x - p.x0_d;
+    uh = (float)u;
+    ul = (float)(u - (double)uh);
 }
 
 // Dynamic shared memory: stage_key[kTile] KeyT | stage_idx[kTile] u32 (PERM) | hist[C] u32
 //                        | stage_fine[kTile] u16 | scratch.
-template <typename KeyT, bool PERM>
-__host__ __device__ constexpr size_t k1_smem_bytes(uint32_t num_coarse) {
-    return (size_t)num_coarse * 4 + (size_t)kTile * sizeof(KeyT) + (PERM ? (size_t)kTile * 4 : 0) +
-           (size_t)kTile * 2 + 512;
+inline size_t k1_smem_bytes(size_t ks, bool perm, uint32_t tile, uint32_t num_coarse) {
+    return (size_t)num_coarse * 8 + (size_t)tile * ks + (perm ? (size_t)tile * 4 : 0) + (size_t)tile * 4 + 512;
 }
 
 // GIVEN = true is the multi-GPU receive side (mlsort_sort_records): the bucket travels with
 // the key, so no prediction is repeated; bucket_in holds global buckets, b_lo is this rank's
 // first bucket and idx_in the global input indices.
-template <typename KeyT, int MPAD, int PRED, bool PERM, bool GIVEN = false>
+template <typename KeyT, int MPAD, int PRED, bool PERM, bool GIVEN, int kTile>
 __global__ void __launch_bounds__(kThreads, 2)
 k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p,
-                     KeyT* __restrict__ part_keys, uint16_t* __restrict__ part_fine,
-                     uint32_t* __restrict__ part_idx, uint16_t* __restrict__ matrix,
+                     KeyT* __restrict__ reg_keys, uint16_t* __restrict__ reg_fine,
+                     uint32_t* __restrict__ reg_idx, uint32_t* __restrict__ cursor,
                      DevStatus* __restrict__ st, const uint32_t* __restrict__ bucket_in = nullptr,
                      const uint32_t* __restrict__ idx_in = nullptr, uint32_t b_lo = 0) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t C = p.num_coarse;
-    // layout: stage_key[kTile] KeyT | stage_idx[kTile] u32 (PERM) | hist[C] u32 | stage_fine[kTile] u16 | scratch
+    // layout: stage_key[kTile] KeyT | stage_idx[kTile] u32 (PERM) | stage_b[kTile] u32 | hist[C] u32
+    //         | gadj[C] i32 | scratch
     KeyT* stage_key = reinterpret_cast<KeyT*>(smem);
     uint32_t* stage_idx = reinterpret_cast<uint32_t*>(smem + (size_t)kTile * sizeof(KeyT));
-    uint32_t* hist = stage_idx + (PERM ? kTile : 0);
-    uint16_t* stage_fine = reinterpret_cast<uint16_t*>(hist + C);
-    uint32_t* scratch = reinterpret_cast<uint32_t*>(stage_fine + kTile);
+    uint32_t* stage_b = stage_idx + (PERM ? kTile : 0);
+    uint32_t* hist = stage_b + kTile;
+    int32_t* gadj = reinterpret_cast<int32_t*>(hist + C);
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(gadj + C);
 
+    constexpr int kKeysPerThread = kTile / kThreads;
     const int tid = threadIdx.x;
     const uint32_t tile = blockIdx.x;
     const uint64_t base = (uint64_t)tile * kTile;
@@ -85,26 +94,49 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
             sb[e] = b < p.bm.Bm1 ? b : p.bm.Bm1;
         }
     }
+    // keys of the next group are loaded while the current group is evaluated
+    KeyT xn[kGroup];
+#pragma unroll
+    for (int q = 0; q < kGroup; ++q) {
+        const uint32_t e = tid + kThreads * q;
+        xn[q] = (!GIVEN && e < cnt) ? keys[base + e] : (KeyT)p.lo_d;
+    }
 #pragma unroll 1
     for (int g = 0; g < (GIVEN ? 0 : kKeysPerThread / kGroup); ++g) {
-        float u[kGroup], y[kGroup];
+        float u[kGroup], ul[kGroup];
+        int32_t y[kGroup];
+        KeyT xc[kGroup];
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) xc[q] = xn[q];
+        if (g + 1 < kKeysPerThread / kGroup) {
+#pragma unroll
+            for (int q = 0; q < kGroup; ++q) {
+                const uint32_t e = tid + kThreads * ((g + 1) * kGroup + q);
+                xn[q] = e < cnt ? keys[base + e] : (KeyT)p.lo_d;
+            }
+        }
 #pragma unroll
         for (int q = 0; q < kGroup; ++q) {
             const uint32_t e = tid + kThreads * (g * kGroup + q);
-            KeyT x = e < cnt ? keys[base + e] : (KeyT)p.lo_d;
+            KeyT x = xc[q];
             if (!KeyTraits<KeyT>::finite(x)) {
                 atomicMin(&st->bad_index, (unsigned long long)(base + e));
                 x = (KeyT)p.lo_d;
             }
             if (e < cnt) {
-                tail_lo += (double)x < p.lo_d;
-                tail_hi += (double)x > p.hi_d;
+                if (sizeof(KeyT) == 4) {
+                    tail_lo += (float)x < p.lo_tf;
+                    tail_hi += (float)x > p.hi_tf;
+                } else {
+                    tail_lo += (double)x < p.lo_d;
+                    tail_hi += (double)x > p.hi_d;
+                }
             }
-            u[q] = key_to_u<KeyT>(x, p);
+            key_to_u<KeyT>(x, p, u[q], ul[q]);
         }
-        gvm_forward_f32<MPAD, PRED, kGroup>(fw, u, y);
+        gvm_forward_fxp<MPAD, PRED, kGroup, sizeof(KeyT) == 8>(fw, u, ul, y);
 #pragma unroll
-        for (int q = 0; q < kGroup; ++q) sb[tid + kThreads * (g * kGroup + q)] = bucket_of(y[q], p.bm);
+        for (int q = 0; q < kGroup; ++q) sb[tid + kThreads * (g * kGroup + q)] = bucket_of_fxp(y[q], p.bm);
     }
     uint32_t bk[kKeysPerThread];
 #pragma unroll
@@ -119,31 +151,31 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
     }
     __syncthreads();
 
-    // ---- exclusive scan of hist; write this tile's column of M (uint16, <= kTile)
+    // ---- exclusive scan of hist; reserve this tile's piece in every coarse bucket's region
     const uint32_t per = (C + kThreads - 1) / kThreads;
     const uint32_t c0 = min(C, tid * per), c1 = min(C, c0 + per);
     uint32_t local = 0;
     for (uint32_t c = c0; c < c1; ++c) local += hist[c];
     uint32_t total;
     uint32_t run = block_exclusive_scan<kThreads>(local, scratch, &total);
-    for (uint32_t c = c0; c < c1; ++c) {
-        uint32_t h = hist[c];
+#pragma unroll 8
+    for (uint32_t c = c0; c < c1; ++c) {        // unrolled: the reservations are issued back to back
+        const uint32_t h = hist[c];
+        const uint32_t g = h ? atomicAdd(&cursor[c], h) : 0u;
+        gadj[c] = (int32_t)g - (int32_t)run;     // region slot of staged element e = gadj[c] + e
         hist[c] = run;
-        matrix[(size_t)c * p.num_tiles + tile] = (uint16_t)run;
         run += h;
     }
-    if (tid == 0) matrix[(size_t)C * p.num_tiles + tile] = (uint16_t)cnt;   // sentinel row
     __syncthreads();
 
     // ---- scatter into the shared staging area, partitioned by coarse id
-    const uint32_t fmask = (1u << p.fine_bits) - 1u;
 #pragma unroll
     for (int k = 0; k < kKeysPerThread; ++k) {
         const uint32_t e = tid + kThreads * k;
         if (e < cnt) {
             const uint32_t pos = atomicAdd(&hist[bk[k] >> p.fine_bits], 1u);
             stage_key[pos] = keys[base + e];            // L2-resident re-read
-            stage_fine[pos] = (uint16_t)(bk[k] & fmask);
+            stage_b[pos] = bk[k];
             if (PERM) stage_idx[pos] = GIVEN ? idx_in[base + e] : (uint32_t)(base + e);
         }
     }
@@ -156,33 +188,44 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
     }
     __syncthreads();
 
-    // ---- coalesced store of the partitioned tile
+    // ---- store every piece into its coarse bucket's region (coalesced within a piece)
+    const uint32_t fmask = (1u << p.fine_bits) - 1u;
+    bool over = false;
     for (uint32_t e = tid; e < cnt; e += kThreads) {
-        part_keys[base + e] = stage_key[e];
-        part_fine[base + e] = stage_fine[e];
-        if (PERM) part_idx[base + e] = stage_idx[e];
+        const uint32_t b = stage_b[e];
+        const uint32_t c = b >> p.fine_bits;
+        const int32_t slot = gadj[c] + (int32_t)e;
+        if ((uint32_t)slot < p.capc) {
+            const size_t dst = (size_t)c * p.capc + (uint32_t)slot;
+            reg_keys[dst] = stage_key[e];
+            reg_fine[dst] = (uint16_t)(b & fmask);
+            if (PERM) reg_idx[dst] = stage_idx[e];
+        } else {
+            over = true;
+        }
     }
+    if (over) atomicAdd(&st->region_overflow, 1ull);
 }
 
-// Column sums of M: S[c] = sum_t M[c][t] = number of keys with coarse id < c, i.e. the
-// global start of coarse bucket c (its length is S[c+1] - S[c]).  One CTA per row.
-__global__ void __launch_bounds__(kThreads)
-k2_coarse_starts(const uint16_t* __restrict__ matrix, uint32_t num_tiles,
-                 unsigned long long* __restrict__ starts) {
-    __shared__ unsigned long long wsum[kWarps];
-    const uint32_t c = blockIdx.x;
-    const uint16_t* row = matrix + (size_t)c * num_tiles;
-    unsigned long long s = 0;
-    for (uint32_t t = threadIdx.x; t < num_tiles; t += kThreads) s += row[t];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+// Global starts of the coarse buckets: exclusive scan of the exact bucket sizes (the final
+// region cursors), one CTA.  starts[C] = n.
+__global__ void __launch_bounds__(1024)
+k2_coarse_starts(const uint32_t* __restrict__ cursor, uint32_t C, unsigned long long* __restrict__ starts) {
+    __shared__ uint32_t scratch[64];
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long t = 0;
-        for (int w = 0; w < kWarps; ++w) t += wsum[w];
-        starts[c] = t;
+    for (uint32_t b0 = 0; b0 < C; b0 += 1024) {
+        const uint32_t c = b0 + threadIdx.x;
+        const uint32_t v = c < C ? cursor[c] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_exclusive_scan<1024>(v, scratch, &tot);
+        if (c < C) starts[c] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
     }
+    if (threadIdx.x == 0) starts[C] = carry;
 }
 
 }  // namespace mlsort

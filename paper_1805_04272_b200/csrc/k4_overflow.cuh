@@ -17,109 +17,45 @@
 
 namespace mlsort {
 
-// ------------------------------------------------------------------ K4 gather
-// Persistent CTAs take big coarse buckets from big_list.  flags[k]: bit0 all keys equal,
-// bit1 run is in input order (every piece was small enough to sort by index).
+// ------------------------------------------------------------------ K4 copy-out
+// Persistent CTAs take big coarse buckets from big_list, copy the bucket's region (K1 left it
+// contiguous) to the bucket's output range and test whether all keys are equal.
+// flags[k] bit0: all keys bit-identical (a key-only run is then final; a perm run only needs
+// its indices sorted).
 template <typename KeyT, bool PERM>
-__global__ void __launch_bounds__(kK3Threads, 1)
-k4_big_gather(uint32_t num_tiles, uint32_t R, const KeyT* __restrict__ part_keys,
-              const uint16_t* __restrict__ part_fine, const uint32_t* __restrict__ part_idx,
-              const uint16_t* __restrict__ matrix, const unsigned long long* __restrict__ starts,
-              KeyT* __restrict__ out_keys, uint32_t* __restrict__ out_perm,
-              unsigned long long* __restrict__ range_start, DevStatus* __restrict__ st,
-              const uint32_t* __restrict__ big_list, uint32_t* __restrict__ flags,
-              unsigned long long* __restrict__ ticket) {
+__global__ void __launch_bounds__(kK3Threads)
+k4_big_copy(uint32_t capc, uint32_t R, const KeyT* __restrict__ reg_keys, const uint32_t* __restrict__ reg_idx,
+            const unsigned long long* __restrict__ starts, KeyT* __restrict__ out_keys,
+            uint32_t* __restrict__ out_perm, unsigned long long* __restrict__ range_start,
+            DevStatus* __restrict__ st, const uint32_t* __restrict__ big_list, uint32_t* __restrict__ flags,
+            unsigned long long* __restrict__ ticket) {
     using Bits = typename KeyTraits<KeyT>::Bits;
-    __shared__ uint32_t scratch[64];
-    __shared__ unsigned long long s_round;
     __shared__ uint32_t s_k;
-    __shared__ int s_unordered;
     __shared__ unsigned long long s_min, s_max;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const unsigned long long nbig = st->big_count;
-    (void)part_fine;
     while (true) {
-        if (tid == 0) s_k = (uint32_t)atomicAdd(ticket, 1ull);
+        if (tid == 0) {
+            s_k = (uint32_t)atomicAdd(ticket, 1ull);
+            s_min = ~0ull;
+            s_max = 0ull;
+        }
         __syncthreads();
         const uint32_t k = s_k;
         if (k >= nbig) return;
         const uint32_t c = big_list[k];
-        const unsigned long long S0 = starts[c];
-        if (tid == 0) {
-            s_round = S0;
-            s_unordered = 0;
-            s_min = ~0ull;
-            s_max = 0ull;
-            range_start[(size_t)c * R] = S0;
-        }
+        const unsigned long long S0 = starts[c], n_c = starts[c + 1] - S0;
+        if (tid == 0) range_start[(size_t)c * R] = S0;
+        const size_t rb0 = (size_t)c * capc;
         Bits vmin = ~(Bits)0, vmax = 0;
-        __syncthreads();
-        const uint16_t* colc = matrix + (size_t)c * num_tiles;
-        const uint16_t* colc1 = matrix + (size_t)(c + 1) * num_tiles;
-        for (uint32_t tr = 0; tr < num_tiles; tr += kK3Threads) {
-            const uint32_t t = tr + warp * 32 + lane;
-            uint32_t off = 0, len = 0;
-            if (t < num_tiles) {
-                off = colc[t];
-                len = (uint32_t)colc1[t] - off;
-            }
-            uint32_t incl = len;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const uint32_t excl = incl - len;
-            const uint32_t wtotal = __shfl_sync(0xffffffffu, incl, 31);
-            uint32_t rtotal;
-            const uint32_t wbase = block_exclusive_scan<kK3Threads>(lane == 31 ? wtotal : 0u, scratch, &rtotal);
-            const unsigned long long base = s_round + __shfl_sync(0xffffffffu, wbase, 31);
-            for (uint32_t b0 = 0; b0 < wtotal; b0 += 32) {
-                const uint32_t i = b0 + lane;
-                int lo = 0;
-#pragma unroll
-                for (int step = 16; step > 0; step >>= 1) {
-                    const int cand = lo + step;
-                    const uint32_t v = __shfl_sync(0xffffffffu, excl, cand & 31);
-                    if (cand < 32 && v <= i) lo = cand;
-                }
-                const uint32_t poff = __shfl_sync(0xffffffffu, off, lo);
-                const uint32_t pexc = __shfl_sync(0xffffffffu, excl, lo);
-                if (i < wtotal) {
-                    const size_t src = (size_t)(tr + warp * 32 + lo) * kTileK3 + poff + (i - pexc);
-                    const KeyT key = part_keys[src];
-                    const Bits ob = KeyTraits<KeyT>::to_ord(key);
-                    vmin = ob < vmin ? ob : vmin;
-                    vmax = ob > vmax ? ob : vmax;
-                    out_keys[base + i] = key;
-                    if (PERM) out_perm[base + i] = part_idx[src];
-                }
-            }
-            if (PERM) {   // each piece comes from one tile (one input-index range): sort it by index
-                __syncwarp();
-                if (len > 64) {
-                    s_unordered = 1;
-                } else if (len > 1) {
-                    const unsigned long long s = base + excl;
-                    for (uint32_t a = 1; a < len; ++a) {
-                        const KeyT kv = out_keys[s + a];
-                        const uint32_t iv = out_perm[s + a];
-                        uint32_t j = a;
-                        while (j > 0 && out_perm[s + j - 1] > iv) {
-                            out_keys[s + j] = out_keys[s + j - 1];
-                            out_perm[s + j] = out_perm[s + j - 1];
-                            --j;
-                        }
-                        out_keys[s + j] = kv;
-                        out_perm[s + j] = iv;
-                    }
-                }
-            }
-            __syncthreads();
-            if (tid == 0) s_round += rtotal;
-            __syncthreads();
+        for (unsigned long long i = tid; i < n_c; i += kK3Threads) {
+            const KeyT key = reg_keys[rb0 + i];
+            const Bits ob = KeyTraits<KeyT>::to_ord(key);
+            vmin = ob < vmin ? ob : vmin;
+            vmax = ob > vmax ? ob : vmax;
+            out_keys[S0 + i] = key;
+            if (PERM) out_perm[S0 + i] = reg_idx[rb0 + i];
         }
-        // all-equal test
         if (vmin != ~(Bits)0) {
             atomicMin(&s_min, (unsigned long long)vmin);
             atomicMax(&s_max, (unsigned long long)vmax);
@@ -127,8 +63,8 @@ k4_big_gather(uint32_t num_tiles, uint32_t R, const KeyT* __restrict__ part_keys
         __syncthreads();
         if (tid == 0) {
             const bool equal = (s_min == s_max);
-            flags[k] = (equal ? 1u : 0u) | (s_unordered ? 0u : 2u);
-            if (!equal || (PERM && s_unordered)) atomicAdd(&st->overflow, 1ull);   // needs K4 radix
+            flags[k] = equal ? 1u : 0u;
+            if (!equal || PERM) atomicAdd(&st->overflow, 1ull);   // needs the K4 radix pass
         }
         __syncthreads();
     }

@@ -2,8 +2,8 @@
 // dispatch and the one host synchronisation per sort.
 //
 // Pipeline of mlsort_sort:
-//   K1 predict + bucket + tile partition      (Eq. 3 l.73-76, l.65)
-//   K2 coarse-bucket starts (column sums of the tile-offset matrix)
+//   K1 predict + bucket + tile partition + region store (Eq. 3 l.73-76, l.65)
+//   K2 coarse-bucket starts (scan of the exact bucket sizes left in the region cursors)
 //   K3 cluster gather + rank-bucket placement + per-bucket fix-up (l.86)
 //   K4 overflow path for coarse buckets K3 cannot hold (l.121 tails)
 //   K5 boundary verify (reading A14) -> conventional-sort fallback on violation
@@ -39,7 +39,8 @@ using namespace mlsort;
 namespace {
 
 constexpr size_t kAlign = 256;
-constexpr size_t kK3SmemBudget = 230400;     // 1 CTA per SM (1024 threads)
+constexpr double kRegionFactor = 4.0;        // region capacity / average coarse-bucket size
+constexpr size_t kK3SmemBudget = 74752;      // three K3 CTAs (256 threads each) per SM
 constexpr int kSMs = 148;
 
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -50,16 +51,39 @@ inline uint32_t ceil_log2(uint64_t x) {
 }
 
 // ---------------------------------------------------------------- folded weights (A1 item 1)
-FoldedWeights fold(const Weights& w, uint32_t mpad) {
+// Fixed-point scale of the y accumulator: |w2_j| 2^S < 2^22 for every neuron (so each
+// rounded term stays in the magic constant's binade) -> S = 21 - floor(log2 max|w2|).
+uint32_t fxp_shift(const Weights& w) {
+    double mx = 0;
+    for (uint32_t j = 0; j < w.m; ++j) mx = std::max(mx, std::fabs(w.w2[j]));
+    if (mx <= 0) return 30;
+    int e = (int)std::floor(std::log2(mx));
+    int S = 21 - e;
+    return (uint32_t)std::max(1, std::min(30, S));
+}
+
+// Origin of u = x - x0 (predict.cuh "Folding"): 0 for f32 keys whose range straddles or is
+// near 0 (u = x exactly), otherwise input_lo.
+double origin_of(const Weights& w, bool f32) {
+    if (!f32) return w.lo;
+    const double span = w.hi - w.lo;
+    if ((w.lo <= 0.0 && w.hi >= 0.0) || std::max(std::fabs(w.lo), std::fabs(w.hi)) <= 4.0 * span) return 0.0;
+    return (double)(float)w.lo;
+}
+
+FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
     FoldedWeights f;
     std::memset(&f, 0, sizeof(f));
     const double log2e = 1.4426950408889634;
     const double span = w.hi - w.lo;
+    const double scale = std::ldexp(1.0, (int)fxp_shift(w));
+    const double x0 = origin_of(w, f32);
     for (uint32_t j = 0; j < mpad; ++j) {
         if (j < w.m) {
-            f.A[j] = (float)(-2.0 * w.beta[j] * w.w1[j] * log2e / span);
-            f.C[j] = (float)(w.beta[j] * (w.w1[j] + w.b[j]) * log2e);
-            f.W[j] = (float)w.w2[j];
+            const double A = -2.0 * w.beta[j] * w.w1[j] * log2e / span;
+            f.A[j] = (float)A;
+            f.C[j] = (float)(w.beta[j] * (w.w1[j] + w.b[j]) * log2e + A * (x0 - w.lo));
+            f.W[j] = (float)(w.w2[j] * scale);
         } else {
             f.A[j] = 0.0f;
             f.C[j] = 0.0f;
@@ -74,13 +98,14 @@ uint32_t mpad_of(uint32_t m) { return m <= 16 ? 16 : m <= 32 ? 32 : 64; }
 // ---------------------------------------------------------------- plan
 struct Plan {
     uint64_t n = 0, B = 0;
-    uint32_t T = 0, fb = 0, C = 0, R = 1, kr = 1, cap = 0;
+    uint32_t tile = kTileSmall;
+    uint32_t T = 0, fb = 0, C = 0, R = 1, kr = 1, cap = 0, capc = 0;
     size_t k1_smem = 0, k3_smem = 0;
     size_t ks = 4;
     bool perm = false;
 };
 
-size_t k3_elem_bytes(size_t ks, bool perm) { return ks * 2 + 2 + (perm ? 8 : 0); }
+size_t k3_elem_bytes(size_t ks, bool perm) { return ks * 2 + 4 + (perm ? 8 : 0); }
 
 Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm) {
     Plan p;
@@ -88,7 +113,8 @@ Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm) {
     p.B = B;
     p.ks = ks;
     p.perm = perm;
-    p.T = (uint32_t)((n + kTile - 1) / kTile);
+    p.tile = kTileSmall;
+    p.T = (uint32_t)((n + p.tile - 1) / p.tile);
     const size_t eb = k3_elem_bytes(ks, perm);
     const uint32_t lb = ceil_log2(B);
     const uint32_t fb_max = std::min<uint32_t>(16, lb);
@@ -96,16 +122,16 @@ Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm) {
     bool found = false;
     for (int fb = (int)fb_max; fb >= (int)fb_min && !found; --fb) {
         const uint64_t C = (B + (1ull << fb) - 1) >> fb;
-        const size_t k1 = (size_t)C * 4 + (size_t)kTile * ks + (perm ? (size_t)kTile * 4 : 0) + kTile * 2 + 512;
+        const size_t k1 = k1_smem_bytes(ks, perm, p.tile, (uint32_t)C);
         if (k1 > 227 * 1024) continue;
         const double avg = (double)n * (double)(1ull << fb) / (double)B;
         for (uint32_t R = 1; R <= 8; R <<= 1) {
             if ((1u << fb) < R) break;
             const uint32_t kr = (1u << fb) / R;
             if (kr > 16384) continue;
-            const long long capll = ((long long)kK3SmemBudget - 256 - 16 - 4ll * kr) / (long long)eb;
+            const long long capll = ((long long)kK3SmemBudget - kCtrlBytes - 16 - 4ll * kr) / (long long)eb;
             if (capll < 64) continue;
-            if (avg <= 0.55 * R * (double)capll) {
+            if (avg <= 0.5 * R * (double)capll) {
                 p.fb = (uint32_t)fb;
                 p.C = (uint32_t)C;
                 p.R = R;
@@ -122,17 +148,23 @@ Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm) {
         p.C = (uint32_t)((B + (1ull << p.fb) - 1) >> p.fb);
         p.R = (1u << p.fb) >= 8 ? 8 : (1u << p.fb);
         p.kr = (1u << p.fb) / p.R;
-        p.cap = (uint32_t)(((long long)kK3SmemBudget - 256 - 16 - 4ll * p.kr) / (long long)eb);
-        p.k1_smem = (size_t)p.C * 4 + (size_t)kTile * ks + (perm ? (size_t)kTile * 4 : 0) + kTile * 2 + 512;
+        p.cap = (uint32_t)(((long long)kK3SmemBudget - kCtrlBytes - 16 - 4ll * p.kr) / (long long)eb);
+        p.k1_smem = k1_smem_bytes(ks, perm, p.tile, p.C);
     }
-    p.k3_smem = 256 + (size_t)p.cap * ks * 2 + (size_t)p.kr * 4 + (perm ? (size_t)p.cap * 8 : 0) + (size_t)p.cap * 2 + 16;
+    {   // region capacity: kRegionFactor x the average coarse bucket, multiple of 8 (16 B rows)
+        const double avg = (double)n * (double)(1ull << p.fb) / (double)B;
+        uint64_t cc = (uint64_t)std::ceil(kRegionFactor * avg) + 64;
+        cc = (cc + 7) & ~7ull;
+        p.capc = (uint32_t)std::min<uint64_t>(cc, 0xFFFFFFF0ull);
+    }
+    p.k3_smem = kCtrlBytes + (size_t)p.cap * ks * 2 + (size_t)p.kr * 4 + (perm ? (size_t)p.cap * 8 : 0) + (size_t)p.cap * 4 + 16;
     return p;
 }
 
 // ---------------------------------------------------------------- workspace layout
 struct Layout {
-    size_t status = 0, part_keys = 0, part_fine = 0, part_idx = 0, matrix = 0, starts = 0,
-           range_start = 0, big_list = 0, flags = 0, radix = 0, total = 0;
+    size_t status = 0, reg_keys = 0, reg_fine = 0, reg_idx = 0, cursor = 0, starts = 0,
+           range_start = 0, big_list = 0, flags = 0, big_mark = 0, radix = 0, total = 0;
     size_t radix_bytes = 0;
 };
 
@@ -150,21 +182,23 @@ Layout make_layout(const Plan& p) {
         return o;
     };
     L.status = take(sizeof(DevStatus));
-    // part_* (K1 -> K3/K4) and the radix area (K4 radix / fallback) are never live together
-    const size_t part_bytes = align_up(p.n * p.ks) + align_up(p.n * 2) + (p.perm ? align_up(p.n * 4) : 0);
+    // regions (K1 -> K3/K4) and the radix area (K4 radix / fallback) are never live together
+    const uint64_t slots = (uint64_t)p.C * p.capc;
+    const size_t reg_bytes = align_up(slots * p.ks) + align_up(slots * 2) + (p.perm ? align_up(slots * 4) : 0);
     const size_t rad = radix_area(p.n, p.ks, p.perm);
-    const size_t shared_area = std::max(part_bytes, rad);
+    const size_t shared_area = std::max(reg_bytes, rad);
     const size_t area = take(shared_area);
-    L.part_keys = area;
-    L.part_fine = area + align_up(p.n * p.ks);
-    L.part_idx = L.part_fine + align_up(p.n * 2);
+    L.reg_keys = area;
+    L.reg_fine = area + align_up(slots * p.ks);
+    L.reg_idx = L.reg_fine + align_up(slots * 2);
     L.radix = area;
     L.radix_bytes = shared_area;
-    L.matrix = take((size_t)(p.C + 1) * p.T * 2);
+    L.cursor = take((size_t)p.C * 4);
     L.starts = take((size_t)(p.C + 1) * 8);
     L.range_start = take((size_t)p.C * p.R * 8);
     L.big_list = take((size_t)p.C * 4);
     L.flags = take((size_t)p.C * 4);
+    L.big_mark = take((size_t)p.C * 4);
     L.total = off;
     return L;
 }
@@ -210,12 +244,12 @@ template <typename KeyT, int MPAD, int PRED, bool PERM, bool GIVEN>
 cudaError_t launch_k1_t(const Plan& p, const KeyT* keys, const FoldedWeights& fw, const K1Params& kp,
                         void* ws, const Layout& L, cudaStream_t s, const uint32_t* bucket_in,
                         const uint32_t* idx_in, uint32_t b_lo) {
-    auto kern = k1_predict_partition<KeyT, MPAD, PRED, PERM, GIVEN>;
+    auto kern = k1_predict_partition<KeyT, MPAD, PRED, PERM, GIVEN, kTileSmall>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k1_smem);
     if (e != cudaSuccess) return e;
-    kern<<<p.T, kThreads, p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.part_keys), at<uint16_t>(ws, L.part_fine),
-                                          PERM ? at<uint32_t>(ws, L.part_idx) : nullptr,
-                                          at<uint16_t>(ws, L.matrix), at<DevStatus>(ws, L.status), bucket_in,
+    kern<<<p.T, kThreads, p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
+                                          PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
+                                          at<uint32_t>(ws, L.cursor), at<DevStatus>(ws, L.status), bucket_in,
                                           idx_in, b_lo);
     return cudaGetLastError();
 }
@@ -243,7 +277,7 @@ cudaError_t launch_k3_t(const Plan& p, void* ws, const Layout& L, KeyT* out_keys
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k3_smem);
     if (e != cudaSuccess) return e;
     K3Params kp;
-    kp.num_tiles = p.T;
+    kp.capc = p.capc;
     kp.num_coarse = p.C;
     kp.owner_shift = p.fb - ceil_log2(p.R);
     kp.kr = p.kr;
@@ -262,13 +296,12 @@ cudaError_t launch_k3_t(const Plan& p, void* ws, const Layout& L, KeyT* out_keys
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, kp, (const KeyT*)at<KeyT>(ws, L.part_keys),
-                              (const uint16_t*)at<uint16_t>(ws, L.part_fine),
-                              (const uint32_t*)(PERM ? at<uint32_t>(ws, L.part_idx) : nullptr),
-                              (const uint16_t*)at<uint16_t>(ws, L.matrix),
+    return cudaLaunchKernelEx(&cfg, kern, kp, (const KeyT*)at<KeyT>(ws, L.reg_keys),
+                              (const uint16_t*)at<uint16_t>(ws, L.reg_fine),
+                              (const uint32_t*)(PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr),
                               (const unsigned long long*)at<unsigned long long>(ws, L.starts), out_keys, out_perm,
                               at<unsigned long long>(ws, L.range_start), at<DevStatus>(ws, L.status),
-                              at<uint32_t>(ws, L.big_list));
+                              at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.big_mark));
 }
 
 template <typename KeyT, bool PERM>
@@ -278,6 +311,7 @@ cudaError_t launch_k3(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, 
         case 2: return launch_k3_t<KeyT, PERM, 2>(p, ws, L, out_keys, out_perm, s);
         case 4: return launch_k3_t<KeyT, PERM, 4>(p, ws, L, out_keys, out_perm, s);
         case 8: return launch_k3_t<KeyT, PERM, 8>(p, ws, L, out_keys, out_perm, s);
+        default: break;
     }
     return cudaErrorInvalidValue;
 }
@@ -287,7 +321,7 @@ cudaError_t launch_k3(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, 
 // then over the key digits.  Returns the buffer index (0/1) holding the result.
 template <typename Bits>
 int radix_sort_pairs(Bits* k0, uint32_t* v0, Bits* k1, uint32_t* v1, uint32_t* ghist, uint64_t n,
-                     bool payload_first, cudaStream_t s, Launches& nl, cudaError_t& err) {
+                     bool payload_first, cudaStream_t s, Launches& nl, cudaError_t& err, bool skip_keys = false) {
     const uint32_t nchunks = (uint32_t)((n + kRadixChunk - 1) / kRadixChunk);
     int cur = 0;
     auto pass = [&](int field, int shift) {
@@ -303,7 +337,8 @@ int radix_sort_pairs(Bits* k0, uint32_t* v0, Bits* k1, uint32_t* v1, uint32_t* g
     };
     if (payload_first && v0)
         for (int sh = 0; sh < 32; sh += 8) pass(1, sh);
-    for (int sh = 0; sh < (int)(sizeof(Bits) * 8); sh += 8) pass(0, sh);
+    if (!skip_keys)
+        for (int sh = 0; sh < (int)(sizeof(Bits) * 8); sh += 8) pass(0, sh);
     err = cudaGetLastError();
     return cur;
 }
@@ -315,7 +350,7 @@ int grid_for(uint64_t n, int threads) {
 
 // Sort segment [S0, S0+len) of (out_keys, out_perm) by (key, index) with the radix area.
 template <typename KeyT, bool PERM>
-int radix_segment(KeyT* out_keys, uint32_t* out_perm, uint64_t S0, uint64_t len, bool input_ordered,
+int radix_segment(KeyT* out_keys, uint32_t* out_perm, uint64_t S0, uint64_t len, bool keys_equal,
                   void* ws, const Layout& L, cudaStream_t s, Launches& nl) {
     using Bits = typename KeyTraits<KeyT>::Bits;
     char* base = at<char>(ws, L.radix);
@@ -327,7 +362,7 @@ int radix_segment(KeyT* out_keys, uint32_t* out_perm, uint64_t S0, uint64_t len,
     k_to_ord<KeyT><<<grid_for(len, 256), 256, 0, s>>>(out_keys + S0, k0, nullptr, len, 0);
     if (PERM) CK(cudaMemcpyAsync(v0, out_perm + S0, len * 4, cudaMemcpyDeviceToDevice, s));
     cudaError_t err;
-    int cur = radix_sort_pairs<Bits>(k0, v0, k1, v1, gh, len, PERM && !input_ordered, s, nl, err);
+    int cur = radix_sort_pairs<Bits>(k0, v0, k1, v1, gh, len, PERM, s, nl, err, keys_equal);
     if (err != cudaSuccess) return MLSORT_ERR_CUDA;
     k_from_ord<KeyT><<<grid_for(len, 256), 256, 0, s>>>(cur ? k1 : k0, out_keys + S0, len);
     if (PERM) CK(cudaMemcpyAsync(out_perm + S0, cur ? v1 : v0, len * 4, cudaMemcpyDeviceToDevice, s));
@@ -358,16 +393,27 @@ int fallback_sort(const KeyT* keys, uint64_t n, KeyT* out_keys, uint32_t* out_pe
     return MLSORT_OK;
 }
 
-K1Params k1_params(const Weights& w, const Plan& p, uint64_t B) {
+K1Params k1_params(const Weights& w, const Plan& p, uint64_t B, bool f32) {
     K1Params kp;
     kp.lo_d = w.lo;
     kp.hi_d = w.hi;
-    kp.lo_f = (float)w.lo;
+    kp.x0_d = origin_of(w, f32);
+    kp.x0_f = (float)kp.x0_d;
+    {   // f32 tail thresholds: smallest float >= lo, largest float <= hi
+        float lf = (float)w.lo, hf = (float)w.hi;
+        if ((double)lf < w.lo) lf = std::nextafter(lf, INFINITY);
+        if ((double)hf > w.hi) hf = std::nextafter(hf, -INFINITY);
+        kp.lo_tf = lf;
+        kp.hi_tf = hf;
+    }
     kp.bm.Bf = (float)B;
     kp.bm.Bm1 = (uint32_t)(B - 1);
+    kp.bm.B = B;
+    kp.bm.S = fxp_shift(w);
     kp.fine_bits = p.fb;
     kp.num_coarse = p.C;
     kp.num_tiles = p.T;
+    kp.capc = p.capc;
     kp.n = p.n;
     return kp;
 }
@@ -421,20 +467,22 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         CK(cudaMemcpyAsync(dst, &init, sizeof(init), cudaMemcpyHostToDevice, s));
     }
     CK(cudaMemsetAsync(at<void>(ws, L.range_start), 0xff, (size_t)p.C * p.R * 8, s));
+    CK(cudaMemsetAsync(at<void>(ws, L.big_mark), 0, (size_t)p.C * 4, s));
+    CK(cudaMemsetAsync(at<void>(ws, L.cursor), 0, (size_t)p.C * 4, s));
 
     FoldedWeights fw;
     uint32_t mpad = 16;
     K1Params kp;
     if (!GIVEN) {
         mpad = mpad_of(w->m);
-        fw = fold(*w, mpad);
-        kp = k1_params(*w, p, B);
+        fw = fold(*w, mpad, sizeof(KeyT) == 4);
+        kp = k1_params(*w, p, B, sizeof(KeyT) == 4);
     } else {
         std::memset(&fw, 0, sizeof(fw));
         Weights dummy;
         dummy.lo = 0;
         dummy.hi = 1;
-        kp = k1_params(dummy, p, B);
+        kp = k1_params(dummy, p, B, sizeof(KeyT) == 4);
         kp.lo_d = -INFINITY;
         kp.hi_d = INFINITY;
     }
@@ -442,14 +490,13 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     tm.start(timing, s);
     CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kp, ws, L, s, bucket_in, idx_in, b_lo)));
     tm.mark();
-    k2_coarse_starts<<<p.C + 1, kThreads, 0, s>>>(at<uint16_t>(ws, L.matrix), p.T, at<unsigned long long>(ws, L.starts));
+    k2_coarse_starts<<<1, 1024, 0, s>>>(at<uint32_t>(ws, L.cursor), p.C, at<unsigned long long>(ws, L.starts));
     CK(cudaGetLastError());
     tm.mark();
     CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s)));
     tm.mark();
-    k4_big_gather<KeyT, PERM><<<num_sms(), kK3Threads, 0, s>>>(
-        p.T, p.R, at<KeyT>(ws, L.part_keys), at<uint16_t>(ws, L.part_fine),
-        PERM ? at<uint32_t>(ws, L.part_idx) : nullptr, at<uint16_t>(ws, L.matrix),
+    k4_big_copy<KeyT, PERM><<<num_sms(), kK3Threads, 0, s>>>(
+        p.capc, p.R, at<KeyT>(ws, L.reg_keys), PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
         at<unsigned long long>(ws, L.starts), out_keys, out_perm, at<unsigned long long>(ws, L.range_start), dst,
         at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.flags), &dst->ticket);
     CK(cudaGetLastError());
@@ -478,7 +525,8 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         return MLSORT_ERR_NONFINITE_KEY;
     }
     uint64_t violations = st.violations;
-    if (st.overflow > 0) {   // K4 radix for big buckets that are not all-equal
+    if (st.region_overflow > 0) violations += 1;   // a region was full: use the conventional sort
+    if (st.region_overflow == 0 && st.overflow > 0) {   // K4 radix for big buckets that are not all-equal
         std::vector<uint32_t> big(st.big_count), flags(st.big_count);
         std::vector<unsigned long long> starts(p.C + 1);
         CK(cudaMemcpyAsync(big.data(), at<uint32_t>(ws, L.big_list), big.size() * 4, cudaMemcpyDeviceToHost, s));
@@ -487,10 +535,10 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
                            cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         for (size_t k = 0; k < big.size(); ++k) {
-            const bool equal = flags[k] & 1u, ordered = flags[k] & 2u;
-            if (equal && (!PERM || ordered)) continue;
+            const bool equal = flags[k] & 1u;
+            if (equal && !PERM) continue;
             const uint64_t S0 = starts[big[k]], len = starts[big[k] + 1] - S0;
-            int rc = radix_segment<KeyT, PERM>(out_keys, out_perm, S0, len, ordered, ws, L, s, nl);
+            int rc = radix_segment<KeyT, PERM>(out_keys, out_perm, S0, len, equal, ws, L, s, nl);
             if (rc) return rc;
         }
         // re-verify every boundary now that all ranges are final
@@ -652,21 +700,22 @@ k_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Params 
     constexpr int G = 8;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * G) {
-        float u[G], y[G];
+        float u[G], ul[G];
+        int32_t y[G];
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             const uint64_t i = i0 + (uint64_t)q * stride;
             KeyT x = i < n ? keys[i] : (KeyT)p.lo_d;
             if (!KeyTraits<KeyT>::finite(x)) x = (KeyT)p.lo_d;
-            u[q] = key_to_u<KeyT>(x, p);
+            key_to_u<KeyT>(x, p, u[q], ul[q]);
         }
-        gvm_forward_f32<MPAD, PRED, G>(fw, u, y);
+        gvm_forward_fxp<MPAD, PRED, G, sizeof(KeyT) == 8>(fw, u, ul, y);
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             const uint64_t i = i0 + (uint64_t)q * stride;
             if (i < n) {
-                if (y_out) y_out[i] = y[q];
-                if (b_out) b_out[i] = bucket_of(y[q], p.bm);
+                if (y_out) y_out[i] = fxp_to_float(y[q], p.bm);
+                if (b_out) b_out[i] = bucket_of_fxp(y[q], p.bm);
             }
         }
     }
@@ -676,10 +725,10 @@ template <typename KeyT>
 int launch_predict(const KeyT* keys, uint64_t n, const Weights& w, uint64_t B, int pred, float* y, uint32_t* b,
                    cudaStream_t s) {
     const uint32_t mpad = mpad_of(w.m);
-    FoldedWeights fw = fold(w, mpad);
+    FoldedWeights fw = fold(w, mpad, sizeof(KeyT) == 4);
     Plan p;
     p.n = n;
-    K1Params kp = k1_params(w, p, B);
+    K1Params kp = k1_params(w, p, B, sizeof(KeyT) == 4);
     const int grid = num_sms() * 8;
 #define PCASE(M)                                                                                    \
     if (mpad == M) {                                                                                \
@@ -750,10 +799,10 @@ extern "C" int mlsort_dist_partition(const void* d_shard, uint64_t n_local, uint
     init.bad_index = ~0ull;
     CK(cudaMemcpyAsync(dst, &init, sizeof(init), cudaMemcpyHostToDevice, s));
     const uint32_t mpad = mpad_of(w->m);
-    FoldedWeights fw = fold(*w, mpad);
+    FoldedWeights fw = fold(*w, mpad, dt == MLSORT_F32);
     Plan p;
     p.n = n_local;
-    K1Params kp = k1_params(*w, p, B);
+    K1Params kp = k1_params(*w, p, B, dt == MLSORT_F32);
     int rc = dt == MLSORT_F32
                  ? dist_partition<float>((const float*)d_shard, n_local, global_offset, B, nranks, mpad, pred, fw, kp,
                                          (float*)d_rec_keys, d_rec_bucket, d_rec_index, bucket_tmp, ghist, dst,

@@ -1,13 +1,15 @@
 // predict.cuh -- the GVM forward pass (§2 Eq. 3, l.73-76) in f32 on the SFU/FMA
 // pipes, and the rank-bucket map r = round(y*B) (l.65).
 //
-// Folding: with u = x - lo and
-// x^ = 2u/(hi-lo) - 1, the logistic argument satisfies
+// Folding: with u = x - x0 and
+// x^ = 2(u + x0 - lo)/(hi-lo) - 1, the logistic argument satisfies
 //     exp(-t_j) = 2^(A_j*u + C_j),   A_j = -2 beta_j w1_j log2(e)/(hi-lo),
-//                                    C_j =  beta_j (w1_j + b_j) log2(e),
-// so one activation is  a = FFMA(A_j, u, C_j); e = ex2(a); d = 1 + e; r = 1/d;
-// y = FFMA(w2_j, r, y).  u is formed in the key's own precision (an f64 subtract for
-// f64 keys) and then rounded to f32, so y depends on x only through a monotone map.
+//                                    C_j =  beta_j (w1_j + b_j) log2(e) + A_j (x0 - lo),
+// so one activation is  a = FFMA(A_j, u, C_j); e = ex2(a); d = 1 + e; r = 1/d; then the
+// w2_j-weighted term is accumulated.  The origin x0 is 0 for f32 keys whose range is near 0
+// (then u = x exactly and no key resolution is lost to a subtraction), else input_lo.  f64 keys
+// form u in f64 and split it into two f32 halves (uh + ul, two FFMAs), so y depends on x only
+// through a monotone map of full resolution.
 #pragma once
 
 #include <cstdint>
@@ -22,12 +24,14 @@ constexpr int kMaxM = 64;
 struct FoldedWeights {
     float A[kMaxM];
     float C[kMaxM];
-    float W[kMaxM];
+    float W[kMaxM];    // w2_j * 2^S (fixed-point accumulation scale, see below)
 };
 
 struct BucketMap {
     float Bf;          // (float)B
     uint32_t Bm1;      // B - 1
+    unsigned long long B;
+    uint32_t S;        // y = acc * 2^-S
 };
 
 __device__ __forceinline__ float ex2_approx(float a) {
@@ -52,39 +56,64 @@ __device__ __forceinline__ float rcp_newton(float d) {
 
 enum { kPredMufu = 1, kPredMixed = 2 };
 
+// Fixed-point accumulation of Eq. 3: every term w2_j * sigma_j is scaled
+// by 2^S (folded into W_j) and rounded to an integer by one FFMA against the magic constant
+// 1.5 * 2^23, whose float bits are then summed in a 32-bit integer:
+//     acc = sum_j bits(FFMA(sigma_j, W_j, 1.5*2^23)) - M * bits(1.5*2^23)  =  sum_j round(w2_j sigma_j 2^S).
+// The sum is exact, every rounding is monotone, so y = acc * 2^-S is monotone in u whenever
+// the MUFU results are; and its resolution 2^-S (S = 21 - floor(log2 max|w2|), typically
+// 2^-26..2^-27) is much finer than an f32 sum near y = 1 (2^-24), which keeps the rank
+// buckets Poisson-like instead of merging up to 2^-24 * B of them.
+constexpr float kFxpMagic = 12582912.0f;            // 1.5 * 2^23
+constexpr int32_t kFxpMagicBits = 0x4B400000;
+
 // Evaluate Eq. 3 for KG keys at once (independent chains give the SFU/FMA pipes ILP).
 // MPAD is the padded neuron count (pad neurons have W = 0).  PRED selects the reciprocal
 // formulation; in kPredMixed one neuron in four uses MUFU.RCP and three use the Newton
 // reciprocal, balancing MUFU (ex2) load against FMA-pipe issue.
-template <int MPAD, int PRED, int KG>
-__device__ __forceinline__ void gvm_forward_f32(const FoldedWeights& fw, const float (&u)[KG],
-                                                float (&y)[KG]) {
+template <int MPAD, int PRED, int KG, bool SPLIT>
+__device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const float (&uh)[KG],
+                                                const float (&ul)[KG], int32_t (&acc)[KG]) {
 #pragma unroll
-    for (int q = 0; q < KG; ++q) y[q] = 0.0f;
+    for (int q = 0; q < KG; ++q) acc[q] = -MPAD * kFxpMagicBits;
 #pragma unroll
-    for (int j = 0; j < MPAD; ++j) {
-        const float A = fw.A[j], C = fw.C[j], W = fw.W[j];
-        const bool use_mufu_rcp = (PRED == kPredMufu) || ((j & 3) == 0);
+    for (int j = 0; j < MPAD; j += 2) {          // neuron pairs: one IADD3 accumulates two terms
+        int32_t t[2][KG];
 #pragma unroll
-        for (int q = 0; q < KG; ++q) {
-            float a = fmaf(A, u[q], C);
-            float r;
-            if (use_mufu_rcp) {
-                r = rcp_approx(1.0f + ex2_approx(a));
-            } else {
-                a = fminf(a, 60.0f);             // keeps d = 1 + 2^a inside Newton's range
-                r = rcp_newton(1.0f + ex2_approx(a));
+        for (int h = 0; h < 2; ++h) {
+            const float A = fw.A[j + h], C = fw.C[j + h], W = fw.W[j + h];
+            const bool use_mufu_rcp = (PRED == kPredMufu) || (((j + h) & 3) == 0);
+#pragma unroll
+            for (int q = 0; q < KG; ++q) {
+                float a = fmaf(A, uh[q], C);
+                if (SPLIT) a = fmaf(A, ul[q], a);    // f64 keys: u = uh + ul carries 48 bits of u
+                float r;
+                if (use_mufu_rcp) {
+                    r = rcp_approx(1.0f + ex2_approx(a));
+                } else {
+                    a = fminf(a, 60.0f);             // keeps d = 1 + 2^a inside Newton's range
+                    r = rcp_newton(1.0f + ex2_approx(a));
+                }
+                t[h][q] = __float_as_int(fmaf(r, W, kFxpMagic));
             }
-            y[q] = fmaf(W, r, y[q]);
         }
+#pragma unroll
+        for (int q = 0; q < KG; ++q) acc[q] += t[0][q] + t[1][q];
     }
 }
 
-// r = clamp(round_half_up(y * B), 0, B - 1) (S:232, S:297-S:298).  For y >= 0
-// round-half-up equals round-half-away-from-zero (reading A6); negative y saturate to 0.
-__device__ __forceinline__ uint32_t bucket_of(float y, const BucketMap& bm) {
-    uint32_t r = __float2uint_rd(fmaf(y, bm.Bf, 0.5f));
-    return r < bm.Bm1 ? r : bm.Bm1;
+// r = clamp(round_half_up(y * B), 0, B - 1) with y = acc * 2^-S, in exact integer arithmetic
+// (S:232, S:297-S:298).  For y >= 0 round-half-up equals round-half-away-
+// from-zero (reading A6); negative y map to bucket 0.
+__device__ __forceinline__ uint32_t bucket_of_fxp(int32_t acc, const BucketMap& bm) {
+    const long long v = (long long)acc * (long long)bm.B + (1ll << (bm.S - 1));
+    if (v < 0) return 0u;
+    const unsigned long long r = (unsigned long long)v >> bm.S;
+    return r < bm.Bm1 ? (uint32_t)r : bm.Bm1;
+}
+
+__device__ __forceinline__ float fxp_to_float(int32_t acc, const BucketMap& bm) {
+    return (float)acc * __int_as_float((127 - (int)bm.S) << 23);
 }
 
 }  // namespace mlsort
