@@ -1,0 +1,114 @@
+"""Multi-process (world size 2, gloo, CPU) tests of the N>1 host logic in
+paper_1805_04272_b200/dist.py: owner ranges, the all-to-all-v exchange in
+source-rank order, global offsets, and that the rank-order concatenation equals the 1-process
+sort.
+
+The two compute steps are injected; here they are test stand-ins built on the ORACLE
+(predict / bucket from oracle/, a stable (key, index) sort) so the exchange logic is checked
+on the CPU without a GPU.  The product path injects the CUDA kernels instead.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import workloads
+from paper_1805_04272_b200 import dist as mdist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_partition_fn(w):
+    def fn(shard, goff, n_global, G, B):
+        keys = shard.numpy()
+        b = oracle.bucket(oracle.predict(w, keys), B).astype(np.int64)
+        owner = (b * G) // B
+        order = np.argsort(owner, kind="stable")            # grouped by owner, input order kept
+        sc = np.bincount(owner, minlength=G).tolist()
+        rk = torch.from_numpy(np.ascontiguousarray(keys[order]))
+        rb = torch.from_numpy(b[order].astype(np.int32))
+        ri = torch.from_numpy((goff + order).astype(np.int32))
+        return rk, rb, ri, sc
+    return fn
+
+
+def _oracle_local_sort_fn(k, b, i, lo, hi):
+    assert bool(((b >= lo) & (b < hi)).all()), "record outside the owner range"
+    ob = oracle.order_bits(k.numpy())
+    idx = i.numpy().astype(np.int64) if i is not None else np.arange(len(ob))
+    order = np.lexsort((idx, ob))
+    return k[torch.from_numpy(order)], (i[torch.from_numpy(order)] if i is not None else None)
+
+
+def _worker(rank, world, port, n_per, dist_name, dtype, with_index, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n_global = n_per * world
+        keys = workloads.generate(dist_name, n_global, 21, dtype)
+        w = workloads.random_monotone_weights(8, 3, lo=float(keys.min()), hi=float(keys.max()), scale=6.0)
+        shard = torch.from_numpy(keys[rank * n_per:(rank + 1) * n_per].copy())
+        res = mdist.sort_dist(shard, rank * n_per, n_global, n_global, _oracle_partition_fn(w),
+                              _oracle_local_sort_fn, with_index=with_index)
+        q.put((rank, res.keys.numpy(), None if res.index is None else res.index.numpy(), res.global_offset,
+               res.send_counts, res.recv_counts))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, n_per, dist_name, dtype, with_index):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_per, dist_name, dtype, with_index, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(out, key=lambda t: t[0])
+
+
+@pytest.mark.parametrize("dist_name,dtype,with_index", [("normal", "f32", True), ("grid4096", "f32", True),
+                                                        ("lognormal", "f64", False)])
+def test_sort_dist_world2_matches_single(dist_name, dtype, with_index):
+    world, n_per = 2, 6000
+    res = _run(world, n_per, dist_name, dtype, with_index)
+    keys = workloads.generate(dist_name, n_per * world, 21, dtype)
+    ref_keys, ref_perm = oracle.sorted_reference(keys)
+    got_keys = np.concatenate([r[1] for r in res])
+    np.testing.assert_array_equal(oracle.order_bits(got_keys), oracle.order_bits(ref_keys))
+    if with_index:
+        got_idx = np.concatenate([r[2] for r in res]).astype(np.uint32)
+        np.testing.assert_array_equal(got_idx, ref_perm)
+    # global offsets are the exclusive scan of the run lengths; counts are consistent
+    assert res[0][3] == 0 and res[1][3] == len(res[0][1])
+    assert sum(res[0][4]) == n_per and sum(res[1][4]) == n_per
+    assert res[0][5][1] == res[1][4][0] and res[1][5][0] == res[0][4][1]
+
+
+def test_owner_range_partitions_buckets():
+    for G in (1, 2, 3, 4, 8):
+        for B in (1, 7, 100, 1 << 20):
+            ranges = [mdist.owner_range(g, G, B) for g in range(G)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == B
+            for (a, b), (c, d) in zip(ranges, ranges[1:]):
+                assert b == c
+            for b in {0, B // 3, B - 1}:
+                g = (b * G) // B
+                lo, hi = ranges[g]
+                assert lo <= b < hi
