@@ -174,7 +174,7 @@ def run_single(args):
     p = w.params()
     dt_keys = torch.float32 if cfg.dtype == "f32" else torch.float64
     d_keys = torch.from_numpy(keys).cuda()
-    pred = {"mufu": 1, "mixed": 2, "default": 0}[args.predictor]
+    pred = {"mufu": 1, "mixed": 2, "packed": 3, "default": 0}[args.predictor]
     sorter = mls.Sorter(cfg.n, dt_keys, cfg.perm, cfg.buckets, pred, timing=True).bind(w)
     out_k = torch.empty_like(d_keys)
     out_p = torch.empty(cfg.n, dtype=torch.int32, device="cuda") if cfg.perm else None
@@ -335,7 +335,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--predictor", default="default", choices=["default", "mufu", "mixed"])
+    ap.add_argument("--predictor", default="default", choices=["default", "mufu", "mixed", "packed"])
     ap.add_argument("--cpu-sample", type=int, default=1 << 21)
     ap.add_argument("--ref-sample", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -54,10 +54,12 @@ typedef enum { MLSORT_F32 = 0, MLSORT_F64 = 1 } mlsort_dtype;
 /* Which f32 formulation of the logistic the predict kernel uses.
  * All meet |y - y_fp64| <= 1e-5; the output sort is bit-exact for every choice. */
 typedef enum {
-    MLSORT_PRED_DEFAULT = 0,   /* library choice (currently MLSORT_PRED_MIXED)                 */
+    MLSORT_PRED_DEFAULT = 0,   /* library choice (currently MLSORT_PRED_PACKED)                */
     MLSORT_PRED_MUFU = 1,      /* ex2 + rcp both on the SFU: 2 MUFU per activation             */
-    MLSORT_PRED_MIXED = 2      /* ex2 on the SFU; reciprocal split between SFU and FMA-pipe
-                                  Newton iterations to balance the two pipes                  */
+    MLSORT_PRED_MIXED = 2,     /* ex2 on the SFU; reciprocal split between SFU and scalar
+                                  FMA-pipe Newton iterations                                   */
+    MLSORT_PRED_PACKED = 3     /* ex2 on the SFU; reciprocal on the FMA pipe with packed f32x2
+                                  instructions (bit-trick seed, modified Newton + cubic step)  */
 } mlsort_predictor;
 
 /* Opaque host-resident GVM parameters {m, w1, w2, b, beta, input_lo, input_hi}

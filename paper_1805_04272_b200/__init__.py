@@ -23,7 +23,7 @@ _LIB_PATH = os.path.join(_HERE, "libmlsort.so")
 _lib = None
 
 F32, F64 = 0, 1
-PRED_DEFAULT, PRED_MUFU, PRED_MIXED = 0, 1, 2
+PRED_DEFAULT, PRED_MUFU, PRED_MIXED, PRED_PACKED = 0, 1, 2, 3
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "I/O error", 3: "weights JSON parse error",
           4: "invalid weights", 5: "non-finite key", 6: "CUDA error", 7: "workspace",

@@ -21,7 +21,8 @@ struct DevStatus {
     unsigned long long overflow;    // big buckets that still need the K4 radix pass
     unsigned long long ticket;      // dynamic CTA ticket (K4 persistent loop)
     unsigned long long region_overflow;   // K1 pieces that did not fit their coarse region
-    unsigned long long pad[6];
+    unsigned long long ticket3;     // dynamic coarse-bucket ticket (K3 local-sort persistent loop)
+    unsigned long long pad[5];
 };
 
 // ---- IEEE-754 totalOrder as unsigned integers (reading A10): negative -> ~bits,

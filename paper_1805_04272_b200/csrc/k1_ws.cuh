@@ -1,0 +1,199 @@
+// k1_ws.cuh -- K1 (v3): warp-specialized, persistent predict + bucket + tile partition.
+//
+// PAPER.md §2: every key's rank is estimated independently by the network (Eq. 3, l.73-76;
+// r = round(y*B), l.65) and the keys are put into their rank buckets (l.86).  On B200 the
+// estimate is SFU/FMA-bound and the partition is latency/LSU-bound, so one CTA per SM runs
+// both concurrently on different warps instead of alternating phases:
+//   * predictor warps (kPredWarps) evaluate the GVM for tile k into bucket buffer sb[k & 1];
+//   * partition warps (kPartWarps) take the previous tile from the other buffer: coarse-id
+//     histogram (shared atomics), scan, one global reservation atomic per non-empty coarse
+//     bucket, stable-by-position staging, and the store of every piece into its coarse
+//     bucket's region (keys, fine ids, input indices) -- the same output contract as
+//     k1_predict_partition (regions contiguous per coarse bucket, cursors = exact sizes).
+// The handoff is a double buffer guarded by named barriers (FULL[i]: predictors -> partition,
+// EMPTY[i]: partition -> predictors), so the SFU never waits for the partition.
+#pragma once
+
+#include "common.cuh"
+#include "predict.cuh"
+#include "k1_partition.cuh"
+
+namespace mlsort {
+
+constexpr int kWsThreads = 1024;
+constexpr int kPredWarps = 24;
+constexpr int kPartWarps = 8;
+constexpr int kPredThreads = kPredWarps * 32;     // 768
+constexpr int kPartThreads = kPartWarps * 32;     // 256
+
+template <typename KeyT> struct WsTile;
+template <> struct WsTile<float> { static constexpr int kKeysPerThread = 16; };
+template <> struct WsTile<double> { static constexpr int kKeysPerThread = 8; };
+
+template <typename KeyT>
+__host__ __device__ constexpr int ws_tile() { return kPredThreads * WsTile<KeyT>::kKeysPerThread; }
+
+// smem: sb[2][T] u32 | stage_key[T] KeyT | hist[C] u32 | gadj[C] i32 | stage_e[T] u16 | scratch
+inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse) {
+    return (size_t)tile * 8 + (size_t)tile * ks + (size_t)num_coarse * 8 + (size_t)tile * 2 + 256;
+}
+
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <typename KeyT, int MPAD, int PRED, bool PERM>
+__global__ void __launch_bounds__(kWsThreads, 1)
+k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restrict__ reg_keys,
+      uint16_t* __restrict__ reg_fine, uint32_t* __restrict__ reg_idx, uint32_t* __restrict__ cursor,
+      DevStatus* __restrict__ st) {
+    constexpr int T = ws_tile<KeyT>();
+    constexpr int KPT = WsTile<KeyT>::kKeysPerThread;
+    constexpr int kGroupWs = 8;
+    enum { kFull0 = 1, kEmpty0 = 3, kPart = 5 };
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* sb = reinterpret_cast<uint32_t*>(smem);                         // [2][T]
+    KeyT* stage_key = reinterpret_cast<KeyT*>(smem + (size_t)T * 8);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (size_t)T * 8 + (size_t)T * sizeof(KeyT));
+    const uint32_t C = p.num_coarse;
+    int32_t* gadj = reinterpret_cast<int32_t*>(hist + C);
+    uint16_t* stage_e = reinterpret_cast<uint16_t*>(gadj + C);
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(
+        (reinterpret_cast<uintptr_t>(stage_e + T) + 15) & ~(uintptr_t)15);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const uint32_t ntiles = p.num_tiles;
+    const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    if (warp < kPredWarps) {
+        // ===================================================== predictor warps
+        uint32_t tail_lo = 0, tail_hi = 0;
+        for (uint32_t k = 0; k < my_tiles; ++k) {
+            const uint32_t tile = blockIdx.x + k * gridDim.x;
+            const uint64_t base = (uint64_t)tile * T;
+            const uint32_t cnt = (uint32_t)min((uint64_t)T, p.n - base);
+            const int buf = k & 1;
+            if (k >= 2) nbar_sync(kEmpty0 + buf, kWsThreads);      // partition released sb[buf]
+            uint32_t* sbb = sb + buf * T;
+#pragma unroll 1
+            for (int g = 0; g < KPT / kGroupWs; ++g) {
+                float u[kGroupWs], ul[kGroupWs];
+                int32_t y[kGroupWs];
+#pragma unroll
+                for (int q = 0; q < kGroupWs; ++q) {
+                    const uint32_t e = tid + kPredThreads * (g * kGroupWs + q);
+                    KeyT x = e < cnt ? keys[base + e] : (KeyT)p.lo_d;
+                    if (!KeyTraits<KeyT>::finite(x)) {
+                        atomicMin(&st->bad_index, (unsigned long long)(base + e));
+                        x = (KeyT)p.lo_d;
+                    }
+                    if (e < cnt) {
+                        if (sizeof(KeyT) == 4) {
+                            tail_lo += (float)x < p.lo_tf;
+                            tail_hi += (float)x > p.hi_tf;
+                        } else {
+                            tail_lo += (double)x < p.lo_d;
+                            tail_hi += (double)x > p.hi_d;
+                        }
+                    }
+                    key_to_u<KeyT>(x, p, u[q], ul[q]);
+                }
+                gvm_forward_fxp<MPAD, PRED, kGroupWs, sizeof(KeyT) == 8>(fw, u, ul, y);
+#pragma unroll
+                for (int q = 0; q < kGroupWs; ++q)
+                    sbb[tid + kPredThreads * (g * kGroupWs + q)] = bucket_of_fxp(y[q], p.bm);
+            }
+            nbar_arrive(kFull0 + buf, kWsThreads);                 // sb[buf] is ready
+        }
+        tail_lo = __reduce_add_sync(0xffffffffu, tail_lo);
+        tail_hi = __reduce_add_sync(0xffffffffu, tail_hi);
+        if (lane == 0) {
+            if (tail_lo) atomicAdd(&st->tail_lo, (unsigned long long)tail_lo);
+            if (tail_hi) atomicAdd(&st->tail_hi, (unsigned long long)tail_hi);
+        }
+        return;
+    }
+
+    // ===================================================== partition warps
+    const int pt = tid - kPredThreads;                 // 0 .. kPartThreads-1
+    const int pw = warp - kPredWarps;
+    const uint32_t fbits = p.fine_bits;
+    const uint32_t fmask = (1u << fbits) - 1u;
+    bool over = false;
+    for (uint32_t k = 0; k < my_tiles; ++k) {
+        const uint32_t tile = blockIdx.x + k * gridDim.x;
+        const uint64_t base = (uint64_t)tile * T;
+        const uint32_t cnt = (uint32_t)min((uint64_t)T, p.n - base);
+        const int buf = k & 1;
+        const uint32_t* sbb = sb + buf * T;
+        for (uint32_t c = pt; c < C; c += kPartThreads) hist[c] = 0u;
+        nbar_sync(kFull0 + buf, kWsThreads);           // predictors finished tile k (also orders the zeroing)
+        // ---- coarse histogram
+#pragma unroll 4
+        for (uint32_t e = pt; e < cnt; e += kPartThreads) atomicAdd(&hist[sbb[e] >> fbits], 1u);
+        nbar_sync(kPart, kPartThreads);
+        // ---- scan (warp rows, conflict-free) + reservation of this tile's piece in every region
+        {
+            const uint32_t chunk = (C + kPartWarps - 1) / kPartWarps;
+            const uint32_t b0 = min(C, (uint32_t)pw * chunk), b1 = min(C, b0 + chunk);
+            uint32_t carry = 0;
+#pragma unroll 4
+            for (uint32_t r = b0; r < b1; r += 32) {
+                const uint32_t c = r + lane;
+                const uint32_t v = c < b1 ? hist[c] : 0u;
+                const uint32_t g = v ? atomicAdd(&cursor[c], v) : 0u;
+                uint32_t x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t yy = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += yy;
+                }
+                const uint32_t ex = carry + x - v;             // exclusive within the warp's chunk
+                if (c < b1) {
+                    hist[c] = ex;
+                    gadj[c] = (int32_t)g - (int32_t)ex;
+                }
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+            if (lane == 0) scratch[pw] = carry;
+            nbar_sync(kPart, kPartThreads);
+            uint32_t add = 0;
+            for (int w = 0; w < pw; ++w) add += scratch[w];
+            if (add)
+                for (uint32_t c = b0 + lane; c < b1; c += 32) {
+                    hist[c] += add;
+                    gadj[c] -= (int32_t)add;
+                }
+        }
+        nbar_sync(kPart, kPartThreads);
+        // ---- stage the tile partitioned by coarse id (position -> original offset e, key)
+#pragma unroll 4
+        for (uint32_t e = pt; e < cnt; e += kPartThreads) {
+            const uint32_t pos = atomicAdd(&hist[sbb[e] >> fbits], 1u);
+            stage_e[pos] = (uint16_t)e;
+            stage_key[pos] = keys[base + e];                   // L2-resident re-read
+        }
+        nbar_sync(kPart, kPartThreads);
+        // ---- store every piece into its coarse bucket's region
+#pragma unroll 4
+        for (uint32_t pos = pt; pos < cnt; pos += kPartThreads) {
+            const uint32_t e = stage_e[pos];
+            const uint32_t b = sbb[e];
+            const uint32_t c = b >> fbits;
+            const int32_t slot = gadj[c] + (int32_t)pos;
+            if ((uint32_t)slot < p.capc) {
+                const size_t dst = (size_t)c * p.capc + (uint32_t)slot;
+                reg_keys[dst] = stage_key[pos];
+                reg_fine[dst] = (uint16_t)(b & fmask);
+                if (PERM) reg_idx[dst] = (uint32_t)(base + e);
+            } else {
+                over = true;
+            }
+        }
+        if (k + 2 < my_tiles) nbar_arrive(kEmpty0 + buf, kWsThreads);   // sb[buf] may be refilled
+        nbar_sync(kPart, kPartThreads);                // stage_* / hist free for the next tile
+    }
+    if (over) atomicAdd(&st->region_overflow, 1ull);
+}
+
+}  // namespace mlsort

@@ -103,8 +103,8 @@ __device__ __forceinline__ void cmpx(typename KeyTraits<KeyT>::Bits* key, uint32
     }
 }
 
-template <typename KeyT, bool PERM>
-__device__ void block_bitonic_sort(typename KeyTraits<KeyT>::Bits* key, uint32_t* idx, uint32_t s, uint32_t e) {
+template <typename KeyT, bool PERM, int NT>
+__device__ void block_bitonic_sort_nt(typename KeyTraits<KeyT>::Bits* key, uint32_t* idx, uint32_t s, uint32_t e) {
     const uint32_t n = e - s;
     uint32_t L = 1;
     while (L < n) L <<= 1;
@@ -112,20 +112,26 @@ __device__ void block_bitonic_sort(typename KeyTraits<KeyT>::Bits* key, uint32_t
     if (PERM) idx += s;
     for (uint32_t k = 2; k <= L; k <<= 1) {
         const uint32_t h = k >> 1;
-        for (uint32_t t = threadIdx.x; t < L / 2; t += kK3Threads) {      // flip step
+        for (uint32_t t = threadIdx.x; t < L / 2; t += NT) {      // flip step
             const uint32_t blk = t / h, i = t - blk * h;
             const uint32_t a = blk * k + i, b = blk * k + k - 1 - i;
             if (b < n) cmpx<KeyT, PERM>(key, idx, a, b);
         }
         __syncthreads();
         for (uint32_t j = h >> 1; j > 0; j >>= 1) {
-            for (uint32_t t = threadIdx.x; t < L / 2; t += kK3Threads) {
+            for (uint32_t t = threadIdx.x; t < L / 2; t += NT) {
                 const uint32_t a = 2 * t - (t & (j - 1)), b = a + j;
                 if (b < n) cmpx<KeyT, PERM>(key, idx, a, b);
             }
             __syncthreads();
         }
     }
+}
+
+template <typename KeyT, bool PERM>
+__device__ __forceinline__ void block_bitonic_sort(typename KeyTraits<KeyT>::Bits* key, uint32_t* idx, uint32_t s,
+                                                   uint32_t e) {
+    block_bitonic_sort_nt<KeyT, PERM, kK3Threads>(key, idx, s, e);
 }
 
 template <typename KeyT, bool PERM, int R>

@@ -20,7 +20,9 @@
 #include "common.cuh"
 #include "predict.cuh"
 #include "k1_partition.cuh"
+#include "k1_ws.cuh"
 #include "k3_sort.cuh"
+#include "k3_local.cuh"
 #include "k4_overflow.cuh"
 #include "dist.cuh"
 
@@ -41,6 +43,8 @@ namespace {
 constexpr size_t kAlign = 256;
 constexpr double kRegionFactor = 4.0;        // region capacity / average coarse-bucket size
 constexpr size_t kK3SmemBudget = 74752;      // three K3 CTAs (256 threads each) per SM
+constexpr size_t kK3LSmemMax = 232448;       // K3 local sort: one 1024-thread CTA per SM (227 KB)
+constexpr size_t kK1SmemMax = 110 * 1024;    // K1: keep two 512-thread CTAs per SM
 constexpr int kSMs = 148;
 
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -93,6 +97,12 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
     return f;
 }
 
+int pred_of(int32_t predictor) {
+    if (predictor == MLSORT_PRED_MUFU) return kPredMufu;
+    if (predictor == MLSORT_PRED_MIXED) return kPredMixed;
+    return kPredPacked;   // MLSORT_PRED_DEFAULT, MLSORT_PRED_PACKED
+}
+
 uint32_t mpad_of(uint32_t m) { return m <= 16 ? 16 : m <= 32 ? 32 : 64; }
 
 // ---------------------------------------------------------------- plan
@@ -103,11 +113,37 @@ struct Plan {
     size_t k1_smem = 0, k3_smem = 0;
     size_t ks = 4;
     bool perm = false;
+    bool local = false;      // K3 = one CTA per coarse bucket (k3_local_sort), else clusters
+    bool ws = false;         // K1 = warp-specialized persistent k1_ws (tile = ws tile), else k1_predict_partition
+    uint32_t kfine = 0;      // rank buckets per coarse bucket (local plan)
 };
 
 size_t k3_elem_bytes(size_t ks, bool perm) { return ks * 2 + 4 + (perm ? 8 : 0); }
 
-Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm) {
+constexpr size_t kK1WsSmemMax = 231424;      // 226 KB
+
+uint32_t ws_tile_of(size_t ks) { return ks == 4 ? (uint32_t)ws_tile<float>() : (uint32_t)ws_tile<double>(); }
+
+Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws);
+
+// Choose the K1 variant after the coarse partition is fixed: the warp-specialized kernel when
+// its shared memory fits (and the caller predicts), else the phase-alternating one.
+Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws = true) {
+    Plan p = make_plan_base(n, B, ks, perm, allow_ws);
+    if (allow_ws) {
+        const uint32_t wt = ws_tile_of(ks);
+        const size_t sm = k1ws_smem_bytes(ks, wt, p.C);
+        if (sm <= kK1WsSmemMax) {
+            p.ws = true;
+            p.tile = wt;
+            p.T = (uint32_t)((n + wt - 1) / wt);
+            p.k1_smem = sm;
+        }
+    }
+    return p;
+}
+
+Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws) {
     Plan p;
     p.n = n;
     p.B = B;
@@ -119,6 +155,34 @@ Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm) {
     const uint32_t lb = ceil_log2(B);
     const uint32_t fb_max = std::min<uint32_t>(16, lb);
     const uint32_t fb_min = lb > 14 ? lb - 14 : 0;   // C <= 16384
+    // Local plan (preferred): the fewest coarse buckets such that one CTA holds a coarse bucket
+    // of 2x the average size in shared memory next to its rank-bucket histogram.
+    for (int fb = (int)fb_max; fb >= (int)fb_min; --fb) {
+        const uint64_t C = (B + (1ull << fb) - 1) >> fb;
+        const size_t k1 = k1_smem_bytes(ks, perm, p.tile, (uint32_t)C);
+        const bool ws_fits = allow_ws && k1ws_smem_bytes(ks, ws_tile_of(ks), (uint32_t)C) <= kK1WsSmemMax;
+        if (k1 > kK1SmemMax && !ws_fits) continue;
+        const uint32_t kfine = 1u << fb;
+        const size_t fixed = kCtrlBytes + (size_t)k3l_hist_words(kfine) * 4;
+        if (fixed >= kK3LSmemMax) continue;
+        const size_t leb = ks + (perm ? 4 : 0);
+        const uint64_t cap = std::min<uint64_t>((kK3LSmemMax - fixed) / leb, 0xFFFF0000ull);
+        const double avg = (double)n * (double)kfine / (double)B;
+        if ((double)cap < 2.0 * avg + 64.0) continue;
+        p.local = true;
+        p.fb = (uint32_t)fb;
+        p.C = (uint32_t)C;
+        p.R = 1;
+        p.kr = kfine;
+        p.kfine = kfine;
+        p.cap = (uint32_t)cap;
+        p.k1_smem = k1;
+        p.k3_smem = k3l_smem_bytes(ks, perm, kfine, (uint32_t)cap);
+        uint64_t cc = (uint64_t)std::ceil(kRegionFactor * avg) + 64;
+        cc = (cc + 7) & ~7ull;
+        p.capc = (uint32_t)std::min<uint64_t>(cc, 0xFFFFFFF0ull);
+        return p;
+    }
     bool found = false;
     for (int fb = (int)fb_max; fb >= (int)fb_min && !found; --fb) {
         const uint64_t C = (B + (1ull << fb) - 1) >> fb;
@@ -254,15 +318,41 @@ cudaError_t launch_k1_t(const Plan& p, const KeyT* keys, const FoldedWeights& fw
     return cudaGetLastError();
 }
 
+template <typename KeyT, int MPAD, int PRED, bool PERM>
+cudaError_t launch_k1_ws_t(const Plan& p, const KeyT* keys, const FoldedWeights& fw, const K1Params& kp, void* ws,
+                           const Layout& L, cudaStream_t s) {
+    auto kern = k1_ws<KeyT, MPAD, PRED, PERM>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k1_smem);
+    if (e != cudaSuccess) return e;
+    const int grid = std::min<int>(num_sms(), (int)p.T);
+    kern<<<grid, kWsThreads, p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
+                                             PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr, at<uint32_t>(ws, L.cursor),
+                                             at<DevStatus>(ws, L.status));
+    return cudaGetLastError();
+}
+
 template <typename KeyT, bool PERM, bool GIVEN>
 cudaError_t launch_k1(const Plan& p, const KeyT* keys, uint32_t mpad, int pred, const FoldedWeights& fw,
                       const K1Params& kp, void* ws, const Layout& L, cudaStream_t s,
                       const uint32_t* bucket_in = nullptr, const uint32_t* idx_in = nullptr, uint32_t b_lo = 0) {
     if (GIVEN) return launch_k1_t<KeyT, 16, kPredMufu, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo);
+    if (!GIVEN && p.ws) {
+#define K1WS(M)                                                                                            \
+        if (mpad == M) {                                                                                   \
+            if (pred == kPredMufu) return launch_k1_ws_t<KeyT, M, kPredMufu, PERM>(p, keys, fw, kp, ws, L, s);   \
+            if (pred == kPredMixed) return launch_k1_ws_t<KeyT, M, kPredMixed, PERM>(p, keys, fw, kp, ws, L, s); \
+            return launch_k1_ws_t<KeyT, M, kPredPacked, PERM>(p, keys, fw, kp, ws, L, s);                   \
+        }
+        K1WS(16) K1WS(32) K1WS(64)
+#undef K1WS
+        return cudaErrorInvalidValue;
+    }
 #define K1CASE(M)                                                                                          \
     if (mpad == M) {                                                                                       \
         if (pred == kPredMufu)                                                                             \
             return launch_k1_t<KeyT, M, kPredMufu, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo); \
+        if (pred == kPredPacked)                                                                           \
+            return launch_k1_t<KeyT, M, kPredPacked, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo); \
         return launch_k1_t<KeyT, M, kPredMixed, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo);    \
     }
     K1CASE(16) K1CASE(32) K1CASE(64)
@@ -305,7 +395,30 @@ cudaError_t launch_k3_t(const Plan& p, void* ws, const Layout& L, KeyT* out_keys
 }
 
 template <typename KeyT, bool PERM>
+cudaError_t launch_k3_local(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm,
+                            cudaStream_t s) {
+    auto kern = k3_local_sort<KeyT, PERM>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k3_smem);
+    if (e != cudaSuccess) return e;
+    K3LParams kp;
+    kp.capc = p.capc;
+    kp.num_coarse = p.C;
+    kp.kfine = p.kfine;
+    kp.cap = p.cap;
+    DevStatus* st = at<DevStatus>(ws, L.status);
+    const int grid = std::min<int>(num_sms(), (int)p.C);
+    kern<<<grid, kL3Threads, p.k3_smem, s>>>(kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
+                                              PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
+                                              at<unsigned long long>(ws, L.starts), out_keys, out_perm,
+                                              at<unsigned long long>(ws, L.range_start), st,
+                                              at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.big_mark),
+                                              &st->ticket3);
+    return cudaGetLastError();
+}
+
+template <typename KeyT, bool PERM>
 cudaError_t launch_k3(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s) {
+    if (p.local) return launch_k3_local<KeyT, PERM>(p, ws, L, out_keys, out_perm, s);
     switch (p.R) {
         case 1: return launch_k3_t<KeyT, PERM, 1>(p, ws, L, out_keys, out_perm, s);
         case 2: return launch_k3_t<KeyT, PERM, 2>(p, ws, L, out_keys, out_perm, s);
@@ -456,7 +569,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
                  const uint32_t* bucket_in, const uint32_t* idx_in, uint32_t b_lo, bool timing = false) {
     Launches nl;
     PhaseTimer tm;
-    const Plan p = make_plan(n, B, sizeof(KeyT), PERM);
+    const Plan p = make_plan(n, B, sizeof(KeyT), PERM, !GIVEN);
     const Layout L = make_layout(p);
     if (ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign)) return MLSORT_ERR_WORKSPACE;
     DevStatus* dst = at<DevStatus>(ws, L.status);
@@ -486,7 +599,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         kp.lo_d = -INFINITY;
         kp.hi_d = INFINITY;
     }
-    if (pred != kPredMufu) pred = kPredMixed;
+    if (pred != kPredMufu && pred != kPredMixed) pred = kPredPacked;
     tm.start(timing, s);
     CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kp, ws, L, s, bucket_in, idx_in, b_lo)));
     tm.mark();
@@ -578,9 +691,11 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     return MLSORT_OK;
 }
 
+// Large enough for both plan flavours (predicting sorts may use k1_ws, the records path not).
 uint64_t workspace_bytes(uint64_t n, mlsort_dtype dt, uint64_t B, bool perm) {
-    const Plan p = make_plan(n, B, dt == MLSORT_F32 ? 4 : 8, perm);
-    return make_layout(p).total;
+    const size_t ks = dt == MLSORT_F32 ? 4 : 8;
+    return std::max(make_layout(make_plan(n, B, ks, perm, true)).total,
+                    make_layout(make_plan(n, B, ks, perm, false)).total);
 }
 
 }  // namespace
@@ -617,7 +732,7 @@ extern "C" int mlsort_sort(const void* d_keys, const uint32_t* d_payload, uint64
     const uint64_t B = (o && o->num_buckets) ? o->num_buckets : n;
     if (B > (1ull << 30)) return MLSORT_ERR_INVALID_ARG;
     const Weights* w = reinterpret_cast<const Weights*>(wh);
-    const int pred = (o && o->predictor == MLSORT_PRED_MUFU) ? kPredMufu : kPredMixed;
+    const int pred = pred_of(o ? o->predictor : 0);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     // align the workspace base
     uintptr_t wsp = reinterpret_cast<uintptr_t>(d_ws);
@@ -733,7 +848,8 @@ int launch_predict(const KeyT* keys, uint64_t n, const Weights& w, uint64_t B, i
 #define PCASE(M)                                                                                    \
     if (mpad == M) {                                                                                \
         if (pred == kPredMufu) k_predict<KeyT, M, kPredMufu><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b); \
-        else k_predict<KeyT, M, kPredMixed><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b);            \
+        else if (pred == kPredMixed) k_predict<KeyT, M, kPredMixed><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b); \
+        else k_predict<KeyT, M, kPredPacked><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b);         \
     }
     PCASE(16) PCASE(32) PCASE(64)
 #undef PCASE
@@ -750,7 +866,7 @@ extern "C" int mlsort_predict(const void* d_keys, uint64_t n, mlsort_dtype dt, c
     const uint64_t B = num_buckets ? num_buckets : n;
     if (B > (1ull << 32)) return MLSORT_ERR_INVALID_ARG;
     const Weights* w = reinterpret_cast<const Weights*>(wh);
-    const int pred = predictor == MLSORT_PRED_MUFU ? kPredMufu : kPredMixed;
+    const int pred = pred_of(predictor);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     return dt == MLSORT_F32 ? launch_predict<float>((const float*)d_keys, n, *w, B, pred, d_y, d_bucket, s)
                             : launch_predict<double>((const double*)d_keys, n, *w, B, pred, d_y, d_bucket, s);
@@ -783,7 +899,7 @@ extern "C" int mlsort_dist_partition(const void* d_shard, uint64_t n_local, uint
     const uint64_t B = (o && o->num_buckets) ? o->num_buckets : n_global;
     if (B > (1ull << 30)) return MLSORT_ERR_INVALID_ARG;
     const Weights* w = reinterpret_cast<const Weights*>(wh);
-    const int pred = (o && o->predictor == MLSORT_PRED_MUFU) ? kPredMufu : kPredMixed;
+    const int pred = pred_of(o ? o->predictor : 0);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     uintptr_t wsp = reinterpret_cast<uintptr_t>(d_ws);
     uintptr_t aligned = (wsp + kAlign - 1) / kAlign * kAlign;

@@ -21,7 +21,7 @@ constexpr int kMaxM = 64;
 
 // Passed by value: lives in the kernel-parameter constant bank, so every FFMA reads its
 // weight operand straight from constant memory (warp-uniform, no LDS).
-struct FoldedWeights {
+struct __align__(16) FoldedWeights {
     float A[kMaxM];
     float C[kMaxM];
     float W[kMaxM];    // w2_j * 2^S (fixed-point accumulation scale, see below)
@@ -54,7 +54,43 @@ __device__ __forceinline__ float rcp_newton(float d) {
     return r;
 }
 
-enum { kPredMufu = 1, kPredMixed = 2 };
+enum { kPredMufu = 1, kPredMixed = 2, kPredPacked = 3 };
+
+// ---- packed-pair (f32x2) formulation --------------------
+// Blackwell's FFMA2/FMUL2 evaluate two neurons per instruction; their B operand can be a
+// uniform register, so neuron constants are read as (A_j, A_j+1) pairs straight from the
+// kernel-parameter bank.  The reciprocal 1/d, d = 1 + 2^a in [1, 2^61], is computed on the FMA
+// pipe as
+//     r0 = bits trick  (0x7EF33400 - bits(d); done on bits(-d) as 0xFEF33400 - bits(-d))
+//     r1 = r0 (k1 - d r0)               k1 = 2.001281198  (modified Newton step, |rel| <= 1.3e-3)
+//     r2 = r1 (1 + e + e^2), e = 1 - d r1   (cubic step, |rel| <= (1.3e-3)^3 + rounding)
+// Host emulation (IEEE fma semantics, scripts/k9_pipes.cu notes): max |r2 d - 1| = 6.2e-8
+// (~1 ulp) and r2 is non-increasing in d over every f32 of [1, 2) (the bit trick is
+// scale-invariant, so that binade covers all of them).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(f32x2 r, float& a, float& b) {
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+constexpr f32x2 kNeg1x2 = 0xBF800000BF800000ull;       // (-1, -1)
+constexpr f32x2 kOne1x2 = 0x3F8000003F800000ull;       // (1, 1)
+constexpr f32x2 kMagicx2 = 0x4B4000004B400000ull;      // (1.5 2^23, 1.5 2^23)
+constexpr f32x2 kK1x2 = 0x400014FE400014FEull;         // (2.001281198, 2.001281198) as f32 bits
+constexpr uint32_t kSeedNeg = 0xFEF33400u;             // 0x7EF33400 + 0x80000000 (seed from bits(-d))
 
 // Fixed-point accumulation of Eq. 3: every term w2_j * sigma_j is scaled
 // by 2^S (folded into W_j) and rounded to an integer by one FFMA against the magic constant
@@ -76,6 +112,36 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
                                                 const float (&ul)[KG], int32_t (&acc)[KG]) {
 #pragma unroll
     for (int q = 0; q < KG; ++q) acc[q] = -MPAD * kFxpMagicBits;
+    if (PRED == kPredPacked) {
+        const f32x2* A2 = reinterpret_cast<const f32x2*>(fw.A);
+        const f32x2* C2 = reinterpret_cast<const f32x2*>(fw.C);
+        const f32x2* W2 = reinterpret_cast<const f32x2*>(fw.W);
+#pragma unroll
+        for (int j = 0; j < MPAD / 2; ++j) {
+#pragma unroll
+            for (int q = 0; q < KG; ++q) {
+                f32x2 a2 = ffma2(pk2(uh[q], uh[q]), A2[j], C2[j]);
+                if (SPLIT) a2 = ffma2(pk2(ul[q], ul[q]), A2[j], a2);
+                float a0, a1;
+                upk2(a2, a0, a1);
+                a0 = fminf(a0, 60.0f);               // d = 1 + 2^a stays finite and normal
+                a1 = fminf(a1, 60.0f);
+                const f32x2 nd2 = ffma2(pk2(ex2_approx(a0), ex2_approx(a1)), kNeg1x2, kNeg1x2);   // -d
+                float n0, n1;
+                upk2(nd2, n0, n1);
+                f32x2 r2 = pk2(__uint_as_float(kSeedNeg - __float_as_uint(n0)),
+                               __uint_as_float(kSeedNeg - __float_as_uint(n1)));
+                r2 = fmul2(r2, ffma2(nd2, r2, kK1x2));                  // modified Newton step
+                const f32x2 e2 = ffma2(nd2, r2, kOne1x2);               // e = 1 - d r1
+                r2 = ffma2(r2, ffma2(e2, e2, e2), r2);                  // r1 (1 + e + e^2)
+                const f32x2 t2 = ffma2(r2, W2[j], kMagicx2);
+                float t0, t1;
+                upk2(t2, t0, t1);
+                acc[q] += __float_as_int(t0) + __float_as_int(t1);
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < MPAD; j += 2) {          // neuron pairs: one IADD3 accumulates two terms
         int32_t t[2][KG];
