@@ -22,7 +22,8 @@ struct DevStatus {
     unsigned long long ticket;      // dynamic CTA ticket (K4 persistent loop)
     unsigned long long region_overflow;   // K1 pieces that did not fit their coarse region
     unsigned long long ticket3;     // dynamic coarse-bucket ticket (K3 local-sort persistent loop)
-    unsigned long long pad[5];
+    unsigned long long local_repairs;   // coarse buckets re-sorted in K3 after an inversion
+    unsigned long long pad[4];
 };
 
 // ---- IEEE-754 totalOrder as unsigned integers (reading A10): negative -> ~bits,

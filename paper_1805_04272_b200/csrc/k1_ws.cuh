@@ -33,30 +33,34 @@ template <> struct WsTile<double> { static constexpr int kKeysPerThread = 8; };
 template <typename KeyT>
 __host__ __device__ constexpr int ws_tile() { return kPredThreads * WsTile<KeyT>::kKeysPerThread; }
 
-// smem: sb[2][T] u32 | stage_key[T] KeyT | hist[C] u32 | gadj[C] i32 | stage_e[T] u16 | scratch
+// smem: sb[2][T] u32 | stage_key[T] KeyT | hist[C'] u32 | gbase[C'] i64 | stage_e[T] u16 | scratch
+// (C' = C rounded up to even so gbase is 8-B aligned)
+__host__ __device__ inline uint32_t k1ws_c2(uint32_t num_coarse) { return (num_coarse + 1u) & ~1u; }
 inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse) {
-    return (size_t)tile * 8 + (size_t)tile * ks + (size_t)num_coarse * 8 + (size_t)tile * 2 + 256;
+    return (size_t)tile * 8 + (size_t)tile * ks + (size_t)k1ws_c2(num_coarse) * 12 + (size_t)tile * 2 + 256;
 }
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <typename KeyT, int MPAD, int PRED, bool PERM>
+// KGW = keys evaluated together per predictor thread (ILP); PARTITION = false skips the
+// partition work (scripts/k1_bench.cu uses it to measure the predictor warps alone).
+template <typename KeyT, int MPAD, int PRED, bool PERM, int KGW = 8, bool PARTITION = true>
 __global__ void __launch_bounds__(kWsThreads, 1)
 k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restrict__ reg_keys,
       uint16_t* __restrict__ reg_fine, uint32_t* __restrict__ reg_idx, uint32_t* __restrict__ cursor,
       DevStatus* __restrict__ st) {
     constexpr int T = ws_tile<KeyT>();
     constexpr int KPT = WsTile<KeyT>::kKeysPerThread;
-    constexpr int kGroupWs = 8;
+    constexpr int kGroupWs = KGW;
     enum { kFull0 = 1, kEmpty0 = 3, kPart = 5 };
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* sb = reinterpret_cast<uint32_t*>(smem);                         // [2][T]
     KeyT* stage_key = reinterpret_cast<KeyT*>(smem + (size_t)T * 8);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (size_t)T * 8 + (size_t)T * sizeof(KeyT));
     const uint32_t C = p.num_coarse;
-    int32_t* gadj = reinterpret_cast<int32_t*>(hist + C);
-    uint16_t* stage_e = reinterpret_cast<uint16_t*>(gadj + C);
+    long long* gbase = reinterpret_cast<long long*>(hist + k1ws_c2(C));   // region slot of position 0
+    uint16_t* stage_e = reinterpret_cast<uint16_t*>(gbase + k1ws_c2(C));
     uint32_t* scratch = reinterpret_cast<uint32_t*>(
         (reinterpret_cast<uintptr_t>(stage_e + T) + 15) & ~(uintptr_t)15);
 
@@ -67,43 +71,61 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
 
     if (warp < kPredWarps) {
         // ===================================================== predictor warps
+        // The (tile, group) sequence is flattened so the keys of the next group -- possibly
+        // the first group of the next tile -- are loaded while the current group is evaluated.
+        constexpr int G = KPT / kGroupWs;                  // groups per tile
         uint32_t tail_lo = 0, tail_hi = 0;
-        for (uint32_t k = 0; k < my_tiles; ++k) {
-            const uint32_t tile = blockIdx.x + k * gridDim.x;
-            const uint64_t base = (uint64_t)tile * T;
+        const uint32_t nsteps = my_tiles * G;
+        KeyT xn[kGroupWs];
+        auto load_group = [&](uint32_t step) {
+            const uint32_t k = step / G, g = step - k * G;
+            const uint64_t base = (uint64_t)(blockIdx.x + k * gridDim.x) * T;
+            const uint32_t cnt = (uint32_t)min((uint64_t)T, p.n - base);
+#pragma unroll
+            for (int q = 0; q < kGroupWs; ++q) {
+                const uint32_t e = tid + kPredThreads * (g * kGroupWs + q);
+                xn[q] = e < cnt ? keys[base + e] : (KeyT)p.lo_d;
+            }
+        };
+        if (nsteps) load_group(0);
+#pragma unroll 1
+        for (uint32_t step = 0; step < nsteps; ++step) {
+            const uint32_t k = step / G, g = step - k * G;
+            const uint64_t base = (uint64_t)(blockIdx.x + k * gridDim.x) * T;
             const uint32_t cnt = (uint32_t)min((uint64_t)T, p.n - base);
             const int buf = k & 1;
-            if (k >= 2) nbar_sync(kEmpty0 + buf, kWsThreads);      // partition released sb[buf]
-            uint32_t* sbb = sb + buf * T;
-#pragma unroll 1
-            for (int g = 0; g < KPT / kGroupWs; ++g) {
-                float u[kGroupWs], ul[kGroupWs];
-                int32_t y[kGroupWs];
+            if (g == 0 && k >= 2) nbar_sync(kEmpty0 + buf, kWsThreads);   // partition released sb[buf]
+            KeyT xc[kGroupWs];
 #pragma unroll
-                for (int q = 0; q < kGroupWs; ++q) {
-                    const uint32_t e = tid + kPredThreads * (g * kGroupWs + q);
-                    KeyT x = e < cnt ? keys[base + e] : (KeyT)p.lo_d;
-                    if (!KeyTraits<KeyT>::finite(x)) {
-                        atomicMin(&st->bad_index, (unsigned long long)(base + e));
-                        x = (KeyT)p.lo_d;
-                    }
-                    if (e < cnt) {
-                        if (sizeof(KeyT) == 4) {
-                            tail_lo += (float)x < p.lo_tf;
-                            tail_hi += (float)x > p.hi_tf;
-                        } else {
-                            tail_lo += (double)x < p.lo_d;
-                            tail_hi += (double)x > p.hi_d;
-                        }
-                    }
-                    key_to_u<KeyT>(x, p, u[q], ul[q]);
+            for (int q = 0; q < kGroupWs; ++q) xc[q] = xn[q];
+            if (step + 1 < nsteps) load_group(step + 1);
+            float u[kGroupWs], ul[kGroupWs];
+            int32_t y[kGroupWs];
+#pragma unroll
+            for (int q = 0; q < kGroupWs; ++q) {
+                const uint32_t e = tid + kPredThreads * (g * kGroupWs + q);
+                KeyT x = xc[q];
+                if (!KeyTraits<KeyT>::finite(x)) {
+                    atomicMin(&st->bad_index, (unsigned long long)(base + e));
+                    x = (KeyT)p.lo_d;
                 }
-                gvm_forward_fxp<MPAD, PRED, kGroupWs, sizeof(KeyT) == 8>(fw, u, ul, y);
-#pragma unroll
-                for (int q = 0; q < kGroupWs; ++q)
-                    sbb[tid + kPredThreads * (g * kGroupWs + q)] = bucket_of_fxp(y[q], p.bm);
+                if (e < cnt) {
+                    if (sizeof(KeyT) == 4) {
+                        tail_lo += (float)x < p.lo_tf;
+                        tail_hi += (float)x > p.hi_tf;
+                    } else {
+                        tail_lo += (double)x < p.lo_d;
+                        tail_hi += (double)x > p.hi_d;
+                    }
+                }
+                key_to_u<KeyT>(x, p, u[q], ul[q]);
             }
-            nbar_arrive(kFull0 + buf, kWsThreads);                 // sb[buf] is ready
+            gvm_forward_fxp<MPAD, PRED, kGroupWs, false>(fw, u, ul, y);
+            uint32_t* sbb = sb + buf * T;
+#pragma unroll
+            for (int q = 0; q < kGroupWs; ++q)
+                sbb[tid + kPredThreads * (g * kGroupWs + q)] = bucket_of_fxp(y[q], p.bm);
+            if (g == G - 1) nbar_arrive(kFull0 + buf, kWsThreads);        // sb[buf] is ready
         }
         tail_lo = __reduce_add_sync(0xffffffffu, tail_lo);
         tail_hi = __reduce_add_sync(0xffffffffu, tail_hi);
@@ -128,14 +150,22 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
         const uint32_t* sbb = sb + buf * T;
         for (uint32_t c = pt; c < C; c += kPartThreads) hist[c] = 0u;
         nbar_sync(kFull0 + buf, kWsThreads);           // predictors finished tile k (also orders the zeroing)
+        if (!PARTITION) {
+            if (k + 2 < my_tiles) nbar_arrive(kEmpty0 + buf, kWsThreads);
+            continue;
+        }
         // ---- coarse histogram
 #pragma unroll 4
         for (uint32_t e = pt; e < cnt; e += kPartThreads) atomicAdd(&hist[sbb[e] >> fbits], 1u);
         nbar_sync(kPart, kPartThreads);
-        // ---- scan (warp rows, conflict-free) + reservation of this tile's piece in every region
+        // ---- scan (warp rows, conflict-free) + reservation of this tile's piece in every region.
+        // gbase[c] = slot of the tile's staged position 0 in the flat region array, so a staged
+        // element at position pos goes to gbase[c] + pos.  A piece that would overflow its
+        // region is redirected to the trash rows after the regions (the call then falls back).
         {
             const uint32_t chunk = (C + kPartWarps - 1) / kPartWarps;
             const uint32_t b0 = min(C, (uint32_t)pw * chunk), b1 = min(C, b0 + chunk);
+            const long long trash = (long long)C * p.capc;
             uint32_t carry = 0;
 #pragma unroll 4
             for (uint32_t r = b0; r < b1; r += 32) {
@@ -151,7 +181,9 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
                 const uint32_t ex = carry + x - v;             // exclusive within the warp's chunk
                 if (c < b1) {
                     hist[c] = ex;
-                    gadj[c] = (int32_t)g - (int32_t)ex;
+                    const bool fits = (unsigned long long)g + v <= p.capc;
+                    over |= !fits;
+                    gbase[c] = (fits ? (long long)c * p.capc + g : trash) - (long long)ex;
                 }
                 carry += __shfl_sync(0xffffffffu, x, 31);
             }
@@ -162,7 +194,7 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
             if (add)
                 for (uint32_t c = b0 + lane; c < b1; c += 32) {
                     hist[c] += add;
-                    gadj[c] -= (int32_t)add;
+                    gbase[c] -= (long long)add;
                 }
         }
         nbar_sync(kPart, kPartThreads);
@@ -179,16 +211,10 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
         for (uint32_t pos = pt; pos < cnt; pos += kPartThreads) {
             const uint32_t e = stage_e[pos];
             const uint32_t b = sbb[e];
-            const uint32_t c = b >> fbits;
-            const int32_t slot = gadj[c] + (int32_t)pos;
-            if ((uint32_t)slot < p.capc) {
-                const size_t dst = (size_t)c * p.capc + (uint32_t)slot;
-                reg_keys[dst] = stage_key[pos];
-                reg_fine[dst] = (uint16_t)(b & fmask);
-                if (PERM) reg_idx[dst] = (uint32_t)(base + e);
-            } else {
-                over = true;
-            }
+            const size_t dst = (size_t)(gbase[b >> fbits] + (long long)pos);
+            reg_keys[dst] = stage_key[pos];
+            reg_fine[dst] = (uint16_t)(b & fmask);
+            if (PERM) reg_idx[dst] = (uint32_t)(base + e);
         }
         if (k + 2 < my_tiles) nbar_arrive(kEmpty0 + buf, kWsThreads);   // sb[buf] may be refilled
         nbar_sync(kPart, kPartThreads);                // stage_* / hist free for the next tile

@@ -8,9 +8,11 @@
 //   2. exclusive scan -> start of every rank bucket                           -- A4
 //   3. placement: every key goes to start[f]++ in shared memory (order-preserving
 //      unsigned key bits; index alongside for perm sorts)                     -- A5
-//   4. fix-up: each rank bucket is sorted by (totalOrder key, input index) -- insertion sort
-//      for small buckets, a block-wide bitonic sort for the rare large ones  -- A6
-//   5. adjacent-pair verify over the whole coarse bucket, coalesced store    -- A7
+//   4. fix-up fused with the store: every element (one thread per position) ranks itself in
+//      its rank bucket by counting the elements that precede it under (totalOrder key, input
+//      index) and writes itself to its final position; large buckets get a block bitonic sort -- A6
+//   5. the maximum of each rank bucket checks the next bucket; an inversion re-sorts the
+//      whole coarse bucket in shared memory                                    -- A7 (A14)
 // While it works on bucket c it has already taken the next ticket and asked the L2 to
 // prefetch that bucket's region (cp.async.bulk.prefetch), so the next bucket's loads hit L2.
 // Placement order inside a rank bucket is arbitrary (atomics); the fix-up compares the
@@ -18,12 +20,14 @@
 #pragma once
 
 #include "common.cuh"
+#include <algorithm>
+
 #include "k3_sort.cuh"
 
 namespace mlsort {
 
 constexpr int kL3Threads = 1024;
-constexpr uint32_t kInsMax = 32;        // rank buckets up to this size: per-thread insertion sort
+constexpr uint32_t kL3RankMax = 64;     // rank buckets up to this size: rank by counting
 constexpr uint32_t kL3BigQ = 48;        // queued larger rank buckets per coarse bucket
 
 struct K3LParams {
@@ -33,11 +37,24 @@ struct K3LParams {
     uint32_t cap;           // largest coarse bucket this kernel holds in shared memory
 };
 
-// histogram words rounded up to 4 so the key array after it is 16-B aligned
-__host__ __device__ inline uint32_t k3l_hist_words(uint32_t kfine) { return (kfine + 3u) & ~3u; }
+// The rank-bucket histogram holds two u16 counters per 32-bit word (a coarse bucket never
+// exceeds 65535 elements here); words rounded up to 4 so the key array after it is 16-B aligned.
+__host__ __device__ inline uint32_t k3l_hist_words(uint32_t kfine) { return ((kfine + 1u) / 2u + 3u) & ~3u; }
 
+// smem: ctrl | hist (u16 pairs) | skey[cap] | sidx[cap] (perm) | sfine[cap] u16
 inline size_t k3l_smem_bytes(size_t ks, bool perm, uint32_t kfine, uint32_t cap) {
-    return kCtrlBytes + (size_t)k3l_hist_words(kfine) * 4 + (size_t)cap * ks + (perm ? (size_t)cap * 4 : 0);
+    return kCtrlBytes + (size_t)k3l_hist_words(kfine) * 4 + (size_t)cap * ks + (perm ? (size_t)cap * 4 : 0) +
+           (size_t)cap * 2;
+}
+
+// largest cap with k3l_smem_bytes(...) <= budget
+inline uint32_t k3l_cap_for(size_t budget, size_t ks, bool perm, uint32_t kfine) {
+    const size_t fixed = kCtrlBytes + (size_t)k3l_hist_words(kfine) * 4;
+    if (budget <= fixed) return 0;
+    const size_t leb = ks + (perm ? 4 : 0) + 2;
+    uint64_t cap = std::min<uint64_t>((budget - fixed) / leb, 65535ull);
+    while (cap > 0 && k3l_smem_bytes(ks, perm, kfine, (uint32_t)cap) > budget) --cap;
+    return (uint32_t)cap;
 }
 
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
@@ -63,15 +80,24 @@ __device__ __forceinline__ void prefetch_bucket(const KeyT* reg_keys, const uint
     if (PERM) prefetch_l2(reg_idx + rb, (uint32_t)(n * 4));
 }
 
-__device__ __forceinline__ void hist_add8(uint32_t* hist, const uint4 v) {
-    atomicAdd(&hist[v.x & 0xffffu], 1u);
-    atomicAdd(&hist[v.x >> 16], 1u);
-    atomicAdd(&hist[v.y & 0xffffu], 1u);
-    atomicAdd(&hist[v.y >> 16], 1u);
-    atomicAdd(&hist[v.z & 0xffffu], 1u);
-    atomicAdd(&hist[v.z >> 16], 1u);
-    atomicAdd(&hist[v.w & 0xffffu], 1u);
-    atomicAdd(&hist[v.w >> 16], 1u);
+// counter f lives in half (f & 1) of word f >> 1
+__device__ __forceinline__ void hist_inc(uint32_t* h2, uint32_t f) { atomicAdd(&h2[f >> 1], 1u << ((f & 1u) << 4)); }
+__device__ __forceinline__ uint32_t hist_inc_ret(uint32_t* h2, uint32_t f) {
+    const uint32_t sh = (f & 1u) << 4;
+    return (atomicAdd(&h2[f >> 1], 1u << sh) >> sh) & 0xffffu;
+}
+__device__ __forceinline__ uint32_t hist_get(const uint32_t* h2, uint32_t f) {
+    return (h2[f >> 1] >> ((f & 1u) << 4)) & 0xffffu;
+}
+__device__ __forceinline__ void hist_add8(uint32_t* h2, const uint4 v) {
+    hist_inc(h2, v.x & 0xffffu);
+    hist_inc(h2, v.x >> 16);
+    hist_inc(h2, v.y & 0xffffu);
+    hist_inc(h2, v.y >> 16);
+    hist_inc(h2, v.z & 0xffffu);
+    hist_inc(h2, v.z >> 16);
+    hist_inc(h2, v.w & 0xffffu);
+    hist_inc(h2, v.w >> 16);
 }
 
 // eight consecutive keys from a 16-B aligned address
@@ -99,17 +125,19 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
               uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_mark, unsigned long long* __restrict__ ticket) {
     using Bits = typename KeyTraits<KeyT>::Bits;
     extern __shared__ __align__(16) unsigned char smem[];
-    // ctrl words: [0] current ticket, [1] next ticket, [2] big-queue count, [8..40) scan
-    // scratch, [64 .. 64+2*kL3BigQ) big-queue (s, e) pairs
+    // ctrl words: [1] next ticket, [2] big-queue count, [8..40) scan scratch,
+    // [64 .. 64+3*kL3BigQ) big-queue (start, end, rank bucket) triples
     uint32_t* ctrl = reinterpret_cast<uint32_t*>(smem);
     uint32_t* scratch = ctrl + 8;
     uint32_t* bigq = ctrl + 64;
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + kCtrlBytes);
-    Bits* skey = reinterpret_cast<Bits*>(hist + k3l_hist_words(p.kfine));
+    uint32_t* h2 = reinterpret_cast<uint32_t*>(smem + kCtrlBytes);          // u16 counter pairs
+    Bits* skey = reinterpret_cast<Bits*>(h2 + k3l_hist_words(p.kfine));
     uint32_t* sidx = reinterpret_cast<uint32_t*>(skey + p.cap);
+    uint16_t* sfine = reinterpret_cast<uint16_t*>(sidx + (PERM ? p.cap : 0));
 
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t C = p.num_coarse;
+    const uint32_t hw = (p.kfine + 1u) / 2u;           // histogram words
     if (tid == 0) {
         const uint32_t t0 = (uint32_t)atomicAdd(ticket, 1ull);
         ctrl[1] = t0;
@@ -118,7 +146,6 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             if (n0 <= p.cap) prefetch_bucket<KeyT, PERM>(reg_keys, reg_fine, reg_idx, (size_t)t0 * p.capc, n0);
         }
     }
-    unsigned long long viol_total = 0;
     while (true) {
         __syncthreads();                       // smem of the previous bucket is free; ctrl[1] visible
         const uint32_t c = ctrl[1];
@@ -160,7 +187,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         const uint32_t* gi = PERM ? reg_idx + rb : nullptr;
 
         // ---- 1. histogram of rank buckets (8 fine ids per 128-bit load; rows are 16-B aligned)
-        for (uint32_t f = tid; f < p.kfine; f += kL3Threads) hist[f] = 0u;
+        for (uint32_t w = tid; w < hw; w += kL3Threads) h2[w] = 0u;
         __syncthreads();
         const uint32_t n8 = n >> 3;
         const uint4* g8 = reinterpret_cast<const uint4*>(gf);
@@ -168,31 +195,32 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             uint32_t i = tid;
             for (; i + kL3Threads < n8; i += 2 * kL3Threads) {      // two loads in flight
                 const uint4 v = __ldg(g8 + i), w = __ldg(g8 + i + kL3Threads);
-                hist_add8(hist, v);
-                hist_add8(hist, w);
+                hist_add8(h2, v);
+                hist_add8(h2, w);
             }
-            if (i < n8) hist_add8(hist, __ldg(g8 + i));
-            for (uint32_t t = (n8 << 3) + tid; t < n; t += kL3Threads) atomicAdd(&hist[gf[t]], 1u);
+            if (i < n8) hist_add8(h2, __ldg(g8 + i));
+            for (uint32_t t = (n8 << 3) + tid; t < n; t += kL3Threads) hist_inc(h2, gf[t]);
         }
         __syncthreads();
-        // ---- 2. exclusive scan of the rank-bucket counts: warp w scans rows of 32 counters
-        // of its contiguous chunk (conflict-free), then the warp totals are scanned.
+        // ---- 2. exclusive scan of the counters: warp w scans rows of 32 words (64 counters) of
+        // its contiguous chunk (conflict-free), then the warp totals are scanned
         {
-            const int warp = tid >> 5;
             constexpr int kW = kL3Threads / 32;
-            const uint32_t chunk = (p.kfine + kW - 1) / kW;
-            const uint32_t b0 = min(p.kfine, (uint32_t)warp * chunk), b1 = min(p.kfine, b0 + chunk);
+            const uint32_t chunk = (hw + kW - 1) / kW;
+            const uint32_t b0 = min(hw, (uint32_t)warp * chunk), b1 = min(hw, b0 + chunk);
             uint32_t carry = 0;
             for (uint32_t r = b0; r < b1; r += 32) {
-                const uint32_t f = r + lane;
-                const uint32_t v = f < b1 ? hist[f] : 0u;
-                uint32_t x = v;
+                const uint32_t w = r + lane;
+                const uint32_t v = w < b1 ? h2[w] : 0u;
+                const uint32_t lo = v & 0xffffu, both = lo + (v >> 16);
+                uint32_t x = both;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
+                    const uint32_t yy = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += yy;
                 }
-                if (f < b1) hist[f] = carry + x - v;             // exclusive within the chunk
+                const uint32_t ex = carry + x - both;               // exclusive prefix of counter 2w
+                if (w < b1) h2[w] = ex | ((ex + lo) << 16);
                 carry += __shfl_sync(0xffffffffu, x, 31);
             }
             if (lane == 0) scratch[warp] = carry;
@@ -202,22 +230,21 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
                 uint32_t x = t;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
+                    const uint32_t yy = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += yy;
                 }
                 if (lane < kW) scratch[lane] = x - t;
             }
             __syncthreads();
             const uint32_t add = scratch[warp];
             if (add)
-                for (uint32_t f = b0 + lane; f < b1; f += 32) hist[f] += add;
+                for (uint32_t w = b0 + lane; w < b1; w += 32) h2[w] += add | (add << 16);
         }
         __syncthreads();
-        // ---- 3. placement into rank-bucket order: groups of 8 (fine ids + keys loaded as
-        // 128-bit vectors, issued before the shared-memory atomics that consume them)
+        // ---- 3. placement into rank-bucket order (fine ids + keys as 128-bit vectors); the fine
+        // id of every position is kept for the fix-up
         {
-            uint32_t i = tid;
-            for (; i < n8; i += kL3Threads) {
+            for (uint32_t i = tid; i < n8; i += kL3Threads) {
                 const uint4 fv = __ldg(g8 + i);
                 KeyT kv[8];
                 load8<KeyT>(gk + 8 * (size_t)i, kv);
@@ -232,74 +259,93 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     const uint32_t f = (fw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
-                    const uint32_t pos = atomicAdd(&hist[f], 1u);
+                    const uint32_t pos = hist_inc_ret(h2, f);
                     skey[pos] = KeyTraits<KeyT>::to_ord(kv[k]);
+                    sfine[pos] = (uint16_t)f;
                     if (PERM) sidx[pos] = iv[k];
                 }
             }
             for (uint32_t t = (n8 << 3) + tid; t < n; t += kL3Threads) {
-                const uint32_t pos = atomicAdd(&hist[gf[t]], 1u);
+                const uint32_t f = gf[t];
+                const uint32_t pos = hist_inc_ret(h2, f);
                 skey[pos] = KeyTraits<KeyT>::to_ord(gk[t]);
+                sfine[pos] = (uint16_t)f;
                 if (PERM) sidx[pos] = gi[t];
             }
         }
-        __syncthreads();                       // hist[f] = end of rank bucket f
-        // ---- 4. fix-up: sort every rank bucket by (key, index)
-        for (uint32_t f = tid; f < p.kfine; f += kL3Threads) {
-            const uint32_t s = f ? hist[f - 1] : 0u, e = hist[f];
+        __syncthreads();                       // counter f = end of rank bucket f
+        // ---- 4. fix-up fused with the store ("only the numbers inside each bucket need to
+        // be sorted"): each position ranks its element inside its rank bucket [s, e) by counting
+        // the elements that precede it under (totalOrder key, index) and writes it to its final
+        // output position; the bucket maximum checks the next non-empty bucket (A14)
+        bool bad = false;
+        for (uint32_t pos = tid; pos < n; pos += kL3Threads) {
+            const uint32_t f = sfine[pos];
+            const uint32_t e = hist_get(h2, f), s = f ? hist_get(h2, f - 1) : 0u;
             const uint32_t len = e - s;
-            if (len <= 1) continue;
-            if (len <= kInsMax) {
-                for (uint32_t i = s + 1; i < e; ++i) {
-                    const Bits kv = skey[i];
-                    const uint32_t iv = PERM ? sidx[i] : 0u;
-                    uint32_t j = i;
-                    while (j > s) {
-                        const Bits kp = skey[j - 1];
-                        const bool gt = PERM ? (kp > kv || (kp == kv && sidx[j - 1] > iv)) : (kp > kv);
-                        if (!gt) break;
-                        skey[j] = kp;
-                        if (PERM) sidx[j] = sidx[j - 1];
-                        --j;
+            const Bits kv = skey[pos];
+            const uint32_t iv = PERM ? sidx[pos] : pos;
+            uint32_t rank = 0;
+            if (len > 1) {
+                if (len > kL3RankMax) {
+                    if (pos == s) {
+                        const uint32_t q = atomicAdd(&ctrl[2], 1u);
+                        if (q < kL3BigQ) {
+                            bigq[3 * q] = s;
+                            bigq[3 * q + 1] = e;
+                            bigq[3 * q + 2] = f;
+                        }
                     }
-                    skey[j] = kv;
-                    if (PERM) sidx[j] = iv;
+                    continue;
                 }
-            } else {
-                const uint32_t q = atomicAdd(&ctrl[2], 1u);
-                if (q < kL3BigQ) {
-                    bigq[2 * q] = s;
-                    bigq[2 * q + 1] = e;
+                for (uint32_t q = s; q < e; ++q) {
+                    const Bits kq = skey[q];
+                    const uint32_t iq = PERM ? sidx[q] : q;
+                    rank += (kq < kv || (kq == kv && iq < iv)) ? 1u : 0u;
+                }
+            }
+            out_keys[S0 + s + rank] = KeyTraits<KeyT>::from_ord(kv);
+            if (PERM) out_perm[S0 + s + rank] = iv;
+            if (rank == len - 1 && e < n) {            // bucket max vs the next non-empty bucket
+                const uint32_t e2 = hist_get(h2, sfine[e]);
+                for (uint32_t q = e; q < e2; ++q) {
+                    const Bits kq = skey[q];
+                    bad |= PERM ? (kq < kv || (kq == kv && sidx[q] < iv)) : (kq < kv);
                 }
             }
         }
         __syncthreads();
-        {
-            const uint32_t nbig = ctrl[2];
-            if (nbig > kL3BigQ) {              // many large rank buckets: sort the whole coarse bucket
-                block_bitonic_sort_nt<KeyT, PERM, kL3Threads>(skey, sidx, 0, n);
-            } else {
-                for (uint32_t q = 0; q < nbig; ++q)
-                    block_bitonic_sort_nt<KeyT, PERM, kL3Threads>(skey, sidx, bigq[2 * q], bigq[2 * q + 1]);
+        // ---- 5. large rank buckets (tails collected in the end buckets, heavy duplicates):
+        // block-wide bitonic sort in shared memory, then store
+        const uint32_t nbig = ctrl[2];
+        if (nbig <= kL3BigQ) {
+            for (uint32_t q = 0; q < nbig; ++q) {
+                const uint32_t s = bigq[3 * q], e = bigq[3 * q + 1];
+                block_bitonic_sort_nt<KeyT, PERM, kL3Threads>(skey, sidx, s, e);
+                for (uint32_t i = s + tid; i < e; i += kL3Threads) {
+                    out_keys[S0 + i] = KeyTraits<KeyT>::from_ord(skey[i]);
+                    if (PERM) out_perm[S0 + i] = sidx[i];
+                }
+                if (tid == 0 && e < n) {               // its maximum vs the next bucket
+                    const Bits kv = skey[e - 1];
+                    const uint32_t iv = PERM ? sidx[e - 1] : 0u;
+                    const uint32_t e2 = hist_get(h2, sfine[e]);
+                    for (uint32_t i = e; i < e2; ++i)
+                        bad |= PERM ? (skey[i] < kv || (skey[i] == kv && sidx[i] < iv)) : (skey[i] < kv);
+                }
             }
         }
-        __syncthreads();
-        // ---- 5. verify adjacent pairs of the whole coarse bucket (A14), coalesced store
-        uint32_t viol = 0;
-        for (uint32_t i = tid; i < n; i += kL3Threads) {
-            const Bits b = skey[i];
-            if (i > 0) {
-                const Bits a = skey[i - 1];
-                const bool ok = PERM ? precedes<KeyT, true>(a, sidx[i - 1], b, sidx[i]) : (a <= b);
-                viol += ok ? 0u : 1u;
+        // ---- 6. an inversion between rank buckets (ulp-level non-monotone network output, or a
+        // non-monotone model), or too many large buckets: sort the whole coarse bucket
+        if (__syncthreads_or(bad) || nbig > kL3BigQ) {
+            block_bitonic_sort_nt<KeyT, PERM, kL3Threads>(skey, sidx, 0, n);
+            for (uint32_t i = tid; i < n; i += kL3Threads) {
+                out_keys[S0 + i] = KeyTraits<KeyT>::from_ord(skey[i]);
+                if (PERM) out_perm[S0 + i] = sidx[i];
             }
-            out_keys[S0 + i] = KeyTraits<KeyT>::from_ord(b);
-            if (PERM) out_perm[S0 + i] = sidx[i];
+            if (tid == 0 && nbig <= kL3BigQ) atomicAdd(&st->local_repairs, 1ull);
         }
-        viol_total += viol;
     }
-    const uint32_t v = __reduce_add_sync(0xffffffffu, (uint32_t)viol_total);
-    if (lane == 0 && v) atomicAdd(&st->violations, (unsigned long long)v);
 }
 
 }  // namespace mlsort

@@ -88,12 +88,23 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
             f.A[j] = (float)A;
             f.C[j] = (float)(w.beta[j] * (w.w1[j] + w.b[j]) * log2e + A * (x0 - w.lo));
             f.W[j] = (float)(w.w2[j] * scale);
+            f.Wn[j] = -f.W[j];
         } else {
             f.A[j] = 0.0f;
             f.C[j] = 0.0f;
             f.W[j] = 0.0f;   // pad neurons contribute nothing
+            f.Wn[j] = 0.0f;
         }
     }
+    auto pair = [](float v) {
+        uint32_t b;
+        std::memcpy(&b, &v, 4);
+        return ((unsigned long long)b << 32) | b;
+    };
+    f.one2 = pair(1.0f);
+    f.k1_2 = pair(2.001281198f);
+    f.magic2 = pair(12582912.0f);
+    f.pad2 = 0;
     return f;
 }
 
@@ -163,10 +174,7 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
         const bool ws_fits = allow_ws && k1ws_smem_bytes(ks, ws_tile_of(ks), (uint32_t)C) <= kK1WsSmemMax;
         if (k1 > kK1SmemMax && !ws_fits) continue;
         const uint32_t kfine = 1u << fb;
-        const size_t fixed = kCtrlBytes + (size_t)k3l_hist_words(kfine) * 4;
-        if (fixed >= kK3LSmemMax) continue;
-        const size_t leb = ks + (perm ? 4 : 0);
-        const uint64_t cap = std::min<uint64_t>((kK3LSmemMax - fixed) / leb, 0xFFFF0000ull);
+        const uint64_t cap = k3l_cap_for(kK3LSmemMax, ks, perm, kfine);
         const double avg = (double)n * (double)kfine / (double)B;
         if ((double)cap < 2.0 * avg + 64.0) continue;
         p.local = true;
@@ -247,7 +255,8 @@ Layout make_layout(const Plan& p) {
     };
     L.status = take(sizeof(DevStatus));
     // regions (K1 -> K3/K4) and the radix area (K4 radix / fallback) are never live together
-    const uint64_t slots = (uint64_t)p.C * p.capc;
+    // C regions of capc slots, plus one tile of trash rows for pieces that overflow a region
+    const uint64_t slots = (uint64_t)p.C * p.capc + p.tile;
     const size_t reg_bytes = align_up(slots * p.ks) + align_up(slots * 2) + (p.perm ? align_up(slots * 4) : 0);
     const size_t rad = radix_area(p.n, p.ks, p.perm);
     const size_t shared_area = std::max(reg_bytes, rad);
@@ -662,7 +671,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         CK(cudaStreamSynchronize(s));
         violations = st.violations + hs->violations;
     }
-    if (info) info->repairs = violations;
+    if (info) info->repairs = violations + st.local_repairs;
     if (violations > 0) {   // reading A14: escalate to the conventional sort
         if (GIVEN) {
             // records path: sort (key, global index) pairs of the received records
@@ -824,7 +833,7 @@ k_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Params 
             if (!KeyTraits<KeyT>::finite(x)) x = (KeyT)p.lo_d;
             key_to_u<KeyT>(x, p, u[q], ul[q]);
         }
-        gvm_forward_fxp<MPAD, PRED, G, sizeof(KeyT) == 8>(fw, u, ul, y);
+        gvm_forward_fxp<MPAD, PRED, G, false>(fw, u, ul, y);
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             const uint64_t i = i0 + (uint64_t)q * stride;

@@ -8,8 +8,8 @@
 // so one activation is  a = FFMA(A_j, u, C_j); e = ex2(a); d = 1 + e; r = 1/d; then the
 // w2_j-weighted term is accumulated.  The origin x0 is 0 for f32 keys whose range is near 0
 // (then u = x exactly and no key resolution is lost to a subtraction), else input_lo.  f64 keys
-// form u in f64 and split it into two f32 halves (uh + ul, two FFMAs), so y depends on x only
-// through a monotone map of full resolution.
+// form u in f64 and round it once to f32, so y depends on x only through the monotone map
+// x -> fl32(x - x0) (k1_partition.cuh key_to_u).
 #pragma once
 
 #include <cstdint>
@@ -25,6 +25,10 @@ struct __align__(16) FoldedWeights {
     float A[kMaxM];
     float C[kMaxM];
     float W[kMaxM];    // w2_j * 2^S (fixed-point accumulation scale, see below)
+    float Wn[kMaxM];   // -W_j (the packed predictor carries -1/d)
+    // (c, c) pairs of the packed predictor's constants, read from the parameter bank (uniform
+    // registers) instead of occupying vector register pairs: 1, k1, 1.5*2^23
+    unsigned long long one2, k1_2, magic2, pad2;
 };
 
 struct BucketMap {
@@ -61,9 +65,13 @@ enum { kPredMufu = 1, kPredMixed = 2, kPredPacked = 3 };
 // uniform register, so neuron constants are read as (A_j, A_j+1) pairs straight from the
 // kernel-parameter bank.  The reciprocal 1/d, d = 1 + 2^a in [1, 2^61], is computed on the FMA
 // pipe as
-//     r0 = bits trick  (0x7EF33400 - bits(d); done on bits(-d) as 0xFEF33400 - bits(-d))
+//     r0 = bits trick  (0x7EF33400 - bits(d); the chain carries -r, whose bits are
+//                       0xFEF33400 - bits(d), so no negation is ever issued)
 //     r1 = r0 (k1 - d r0)               k1 = 2.001281198  (modified Newton step, |rel| <= 1.3e-3)
 //     r2 = r1 (1 + e + e^2), e = 1 - d r1   (cubic step, |rel| <= (1.3e-3)^3 + rounding)
+// and the term is FFMA2(-r2, -W, magic).  Every f32x2 constant is a kernel parameter, so the
+// FFMA2s read it from a uniform register instead of a vector register pair (the f32x2 chain is
+// bound by vector-register reads; scripts/k9_pipes.cu measures the variants).
 // Host emulation (IEEE fma semantics, scripts/k9_pipes.cu notes): max |r2 d - 1| = 6.2e-8
 // (~1 ulp) and r2 is non-increasing in d over every f32 of [1, 2) (the bit trick is
 // scale-invariant, so that binade covers all of them).
@@ -81,16 +89,17 @@ __device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
     return d;
 }
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
 __device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
     f32x2 d;
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
 }
-constexpr f32x2 kNeg1x2 = 0xBF800000BF800000ull;       // (-1, -1)
-constexpr f32x2 kOne1x2 = 0x3F8000003F800000ull;       // (1, 1)
-constexpr f32x2 kMagicx2 = 0x4B4000004B400000ull;      // (1.5 2^23, 1.5 2^23)
-constexpr f32x2 kK1x2 = 0x400014FE400014FEull;         // (2.001281198, 2.001281198) as f32 bits
-constexpr uint32_t kSeedNeg = 0xFEF33400u;             // 0x7EF33400 + 0x80000000 (seed from bits(-d))
+constexpr uint32_t kSeedNeg = 0xFEF33400u;             // 0x7EF33400 + 0x80000000: bits of -r0 from bits(d)
 
 // Fixed-point accumulation of Eq. 3: every term w2_j * sigma_j is scaled
 // by 2^S (folded into W_j) and rounded to an integer by one FFMA against the magic constant
@@ -111,11 +120,12 @@ template <int MPAD, int PRED, int KG, bool SPLIT>
 __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const float (&uh)[KG],
                                                 const float (&ul)[KG], int32_t (&acc)[KG]) {
 #pragma unroll
-    for (int q = 0; q < KG; ++q) acc[q] = -MPAD * kFxpMagicBits;
+    // modular (uint32) arithmetic: the partial sums wrap, the final value fits an int32
+    for (int q = 0; q < KG; ++q) acc[q] = (int32_t)(0u - (uint32_t)MPAD * (uint32_t)kFxpMagicBits);
     if (PRED == kPredPacked) {
         const f32x2* A2 = reinterpret_cast<const f32x2*>(fw.A);
         const f32x2* C2 = reinterpret_cast<const f32x2*>(fw.C);
-        const f32x2* W2 = reinterpret_cast<const f32x2*>(fw.W);
+        const f32x2* Wn2 = reinterpret_cast<const f32x2*>(fw.Wn);
 #pragma unroll
         for (int j = 0; j < MPAD / 2; ++j) {
 #pragma unroll
@@ -126,22 +136,22 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
                 upk2(a2, a0, a1);
                 a0 = fminf(a0, 60.0f);               // d = 1 + 2^a stays finite and normal
                 a1 = fminf(a1, 60.0f);
-                const f32x2 nd2 = ffma2(pk2(ex2_approx(a0), ex2_approx(a1)), kNeg1x2, kNeg1x2);   // -d
-                float n0, n1;
-                upk2(nd2, n0, n1);
-                f32x2 r2 = pk2(__uint_as_float(kSeedNeg - __float_as_uint(n0)),
-                               __uint_as_float(kSeedNeg - __float_as_uint(n1)));
-                r2 = fmul2(r2, ffma2(nd2, r2, kK1x2));                  // modified Newton step
-                const f32x2 e2 = ffma2(nd2, r2, kOne1x2);               // e = 1 - d r1
-                r2 = ffma2(r2, ffma2(e2, e2, e2), r2);                  // r1 (1 + e + e^2)
-                const f32x2 t2 = ffma2(r2, W2[j], kMagicx2);
+                const f32x2 d2 = fadd2(pk2(ex2_approx(a0), ex2_approx(a1)), fw.one2);   // d = 1 + e
+                float d0, d1;
+                upk2(d2, d0, d1);
+                // the seed's bit trick yields -r0 directly (sign bit folded into the constant)
+                f32x2 nr2 = pk2(__uint_as_float(kSeedNeg - __float_as_uint(d0)),
+                                __uint_as_float(kSeedNeg - __float_as_uint(d1)));
+                nr2 = fmul2(nr2, ffma2(d2, nr2, fw.k1_2));              // -r1 = -r0 (k1 - d r0)
+                const f32x2 e2 = ffma2(d2, nr2, fw.one2);               // e = 1 - d r1
+                nr2 = ffma2(nr2, ffma2(e2, e2, e2), nr2);               // -r1 (1 + e + e^2)
+                const f32x2 t2 = ffma2(nr2, Wn2[j], fw.magic2);         // W r + magic
                 float t0, t1;
                 upk2(t2, t0, t1);
-                acc[q] += __float_as_int(t0) + __float_as_int(t1);
+                acc[q] = (int32_t)((uint32_t)acc[q] + __float_as_uint(t0) + __float_as_uint(t1));
             }
         }
-        return;
-    }
+    } else {
 #pragma unroll
     for (int j = 0; j < MPAD; j += 2) {          // neuron pairs: one IADD3 accumulates two terms
         int32_t t[2][KG];
@@ -164,7 +174,8 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
             }
         }
 #pragma unroll
-        for (int q = 0; q < KG; ++q) acc[q] += t[0][q] + t[1][q];
+        for (int q = 0; q < KG; ++q) acc[q] = (int32_t)((uint32_t)acc[q] + (uint32_t)t[0][q] + (uint32_t)t[1][q]);
+    }
     }
 }
 

@@ -239,3 +239,49 @@ def test_full_config_sampled(mls, name):
     sub = keys[pos]
     y, b = mls.predict(_t(sub), w, num_buckets=cfg.buckets)
     assert np.max(np.abs(y.cpu().numpy() - oracle.predict(p, sub))) <= 1e-5
+
+
+# ------------------------------------------------------------------ K8: exhaustive monotonicity
+
+def _all_finite_f32_ascending(chunk_bits):
+    """Yield CUDA float32 tensors covering every finite f32 in ascending order (negatives from
+    -FLT_MAX to -0, then +0 to FLT_MAX), chunk by chunk."""
+    import torch
+    neg_hi, pos_hi = 0xFF7FFFFF, 0x7F7FFFFF
+    # negatives: bit patterns descending 0xFF7FFFFF .. 0x80000000
+    start = neg_hi
+    while start >= 0x80000000:
+        n = min(chunk_bits, start - 0x80000000 + 1)
+        b = torch.arange(start, start - n, -1, dtype=torch.int64, device="cuda")
+        yield (b - (1 << 32)).to(torch.int32).view(torch.float32)     # two's-complement bit patterns
+        start -= n
+    start = 0
+    while start <= pos_hi:
+        n = min(chunk_bits, pos_hi - start + 1)
+        b = torch.arange(start, start + n, dtype=torch.int64, device="cuda")
+        yield b.to(torch.int32).view(torch.float32)
+        start += n
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("pred", [0, 1, 2])
+def test_k8_predictor_monotone_over_all_f32(mls, pred):
+    """SURVEY §8(c) pin "predictor y (GPU side): exhaustive monotonicity of K1 over all finite
+    f32 u": with sign-feasible (Eq. 4) weights the device network output and bucket are
+    non-decreasing over every finite float32 key in ascending order (~4.28e9 keys).  f64 keys
+    reach the network only through fl32(x - lo), so this covers them too."""
+    import torch
+    cfg = workloads.CONFIGS["C2"]
+    keys = workloads.generate_config(cfg, n=1 << 18)
+    w, _ = _fit(mls, keys, cfg.m, n0=1 << 14, seed=cfg.train_seed)
+    assert w.check_monotone()
+    last_y, last_b, total = None, None, 0
+    for x in _all_finite_f32_ascending(1 << 28):
+        y, b = mls.predict(x, w, num_buckets=1 << 26, predictor=pred)
+        assert bool((y[1:] >= y[:-1]).all()), "network output decreases somewhere"
+        assert bool((b[1:] >= b[:-1]).all()), "bucket decreases somewhere"
+        if last_y is not None:
+            assert float(y[0]) >= last_y and int(b[0]) >= last_b
+        last_y, last_b = float(y[-1]), int(b[-1])
+        total += x.numel()
+    assert total == 2 * 0x7F800000
