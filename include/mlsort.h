@@ -69,7 +69,9 @@ typedef struct mlsort_weights mlsort_weights;
 typedef struct {
     uint64_t num_buckets;   /* B, the number of rank buckets; 0 means B = n          */
     int32_t  predictor;     /* mlsort_predictor                                             */
-    int32_t  verify;        /* 1 (default) = run the final boundary verify/repair pass      */
+    int32_t  verify;        /* 0/1 (default): every coarse-bucket boundary is verified (K5),
+                               rank-bucket boundaries only when the weights are not
+                               sign-feasible (Eq. 4); 2: verify every rank-bucket boundary  */
     int32_t  timing;        /* 1 = record CUDA events around each kernel phase and report
                                the device times in mlsort_info.phase_ms (bench/profiling)     */
     int32_t  reserved[3];   /* must be zero                                                 */

@@ -23,7 +23,9 @@ struct DevStatus {
     unsigned long long region_overflow;   // K1 pieces that did not fit their coarse region
     unsigned long long ticket3;     // dynamic coarse-bucket ticket (K3 local-sort persistent loop)
     unsigned long long local_repairs;   // coarse buckets re-sorted in K3 after an inversion
-    unsigned long long pad[4];
+    unsigned long long mid_count;   // coarse buckets handed from the primary to the secondary K3 pass
+    unsigned long long ticket3b;    // ticket of the secondary K3 pass
+    unsigned long long pad[2];
 };
 
 // ---- IEEE-754 totalOrder as unsigned integers (reading A10): negative -> ~bits,

@@ -43,7 +43,8 @@ namespace {
 constexpr size_t kAlign = 256;
 constexpr double kRegionFactor = 4.0;        // region capacity / average coarse-bucket size
 constexpr size_t kK3SmemBudget = 74752;      // three K3 CTAs (256 threads each) per SM
-constexpr size_t kK3LSmemMax = 232448;       // K3 local sort: one 1024-thread CTA per SM (227 KB)
+constexpr size_t kK3LSmemMax = 232448;       // K3 secondary pass: one 1024-thread CTA per SM (227 KB)
+constexpr size_t kK3LSmemPrimary = 115712;   // K3 primary pass: two 512-thread CTAs per SM (113 KB each)
 constexpr size_t kK1SmemMax = 110 * 1024;    // K1: keep two 512-thread CTAs per SM
 constexpr int kSMs = 148;
 
@@ -101,6 +102,18 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
         std::memcpy(&b, &v, 4);
         return ((unsigned long long)b << 32) | b;
     };
+    // safe range of u for the clamp-free predictor: a_j = A_j u + C_j <= 59 for every neuron
+    // (the f32 FFMA's rounding is far below the 59 -> 125 margin of the reciprocal chain)
+    double ulo = -INFINITY, uhi = INFINITY;
+    for (uint32_t j = 0; j < mpad; ++j) {
+        const double A = f.A[j], C = f.C[j];
+        if (A < 0) ulo = std::max(ulo, (59.0 - C) / A);
+        else if (A > 0) uhi = std::min(uhi, (59.0 - C) / A);
+        else if (C > 59.0) { ulo = INFINITY; uhi = -INFINITY; }
+    }
+    f.u_safe_lo = ulo == -INFINITY ? -INFINITY : (float)std::nextafter((float)ulo, INFINITY);
+    f.u_safe_hi = uhi == INFINITY ? INFINITY : (float)std::nextafter((float)uhi, -INFINITY);
+    if (!(f.u_safe_lo <= f.u_safe_hi)) { f.u_safe_lo = INFINITY; f.u_safe_hi = -INFINITY; }
     f.one2 = pair(1.0f);
     f.k1_2 = pair(2.001281198f);
     f.magic2 = pair(12582912.0f);
@@ -125,6 +138,8 @@ struct Plan {
     size_t ks = 4;
     bool perm = false;
     bool local = false;      // K3 = one CTA per coarse bucket (k3_local_sort), else clusters
+    uint32_t cap1 = 0;       // local plan: primary-pass capacity (two CTAs per SM)
+    size_t k3_smem1 = 0;     // local plan: primary-pass shared memory
     bool ws = false;         // K1 = warp-specialized persistent k1_ws (tile = ws tile), else k1_predict_partition
     uint32_t kfine = 0;      // rank buckets per coarse bucket (local plan)
 };
@@ -186,6 +201,10 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
         p.cap = (uint32_t)cap;
         p.k1_smem = k1;
         p.k3_smem = k3l_smem_bytes(ks, perm, kfine, (uint32_t)cap);
+        // two-CTA primary pass only when it holds the average bucket with margin
+        p.cap1 = k3l_cap_for(kK3LSmemPrimary, ks, perm, kfine);
+        if ((double)p.cap1 < 1.25 * avg + 64.0) p.cap1 = 0;
+        p.k3_smem1 = p.cap1 ? k3l_smem_bytes(ks, perm, kfine, p.cap1) : 0;
         uint64_t cc = (uint64_t)std::ceil(kRegionFactor * avg) + 64;
         cc = (cc + 7) & ~7ull;
         p.capc = (uint32_t)std::min<uint64_t>(cc, 0xFFFFFFF0ull);
@@ -236,7 +255,7 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
 // ---------------------------------------------------------------- workspace layout
 struct Layout {
     size_t status = 0, reg_keys = 0, reg_fine = 0, reg_idx = 0, cursor = 0, starts = 0,
-           range_start = 0, big_list = 0, flags = 0, big_mark = 0, radix = 0, total = 0;
+           range_start = 0, big_list = 0, flags = 0, big_mark = 0, radix = 0, mid_list = 0, total = 0;
     size_t radix_bytes = 0;
 };
 
@@ -272,6 +291,7 @@ Layout make_layout(const Plan& p) {
     L.big_list = take((size_t)p.C * 4);
     L.flags = take((size_t)p.C * 4);
     L.big_mark = take((size_t)p.C * 4);
+    L.mid_list = take((size_t)p.C * 4);
     L.total = off;
     return L;
 }
@@ -403,31 +423,51 @@ cudaError_t launch_k3_t(const Plan& p, void* ws, const Layout& L, KeyT* out_keys
                               at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.big_mark));
 }
 
-template <typename KeyT, bool PERM>
-cudaError_t launch_k3_local(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm,
-                            cudaStream_t s) {
-    auto kern = k3_local_sort<KeyT, PERM>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k3_smem);
+template <typename KeyT, bool PERM, int NT>
+cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s,
+                           bool verify_fine, bool secondary, bool to_mid, uint32_t cap, size_t smem, int grid) {
+    auto kern = k3_local_sort<KeyT, PERM, NT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     K3LParams kp;
     kp.capc = p.capc;
     kp.num_coarse = p.C;
     kp.kfine = p.kfine;
-    kp.cap = p.cap;
+    kp.cap = cap;
+    kp.verify = verify_fine ? 1u : 0u;
+    kp.secondary = secondary ? 1u : 0u;
+    kp.to_mid = to_mid ? 1u : 0u;
     DevStatus* st = at<DevStatus>(ws, L.status);
-    const int grid = std::min<int>(num_sms(), (int)p.C);
-    kern<<<grid, kL3Threads, p.k3_smem, s>>>(kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
-                                              PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
-                                              at<unsigned long long>(ws, L.starts), out_keys, out_perm,
-                                              at<unsigned long long>(ws, L.range_start), st,
-                                              at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.big_mark),
-                                              &st->ticket3);
+    kern<<<grid, NT, smem, s>>>(kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
+                                PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr, at<unsigned long long>(ws, L.starts),
+                                out_keys, out_perm, at<unsigned long long>(ws, L.range_start), st,
+                                at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.big_mark), at<uint32_t>(ws, L.mid_list),
+                                secondary ? &st->ticket3b : &st->ticket3);
     return cudaGetLastError();
 }
 
+// K3 local plan: primary pass (two 512-thread CTAs per SM, capacity cap1) over every coarse
+// bucket, then the secondary pass (one 1024-thread CTA per SM, capacity cap) over the buckets
+// the primary pass handed over.
 template <typename KeyT, bool PERM>
-cudaError_t launch_k3(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s) {
-    if (p.local) return launch_k3_local<KeyT, PERM>(p, ws, L, out_keys, out_perm, s);
+cudaError_t launch_k3_local(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm,
+                            cudaStream_t s, bool verify_fine) {
+    cudaError_t e;
+    if (p.cap1 > 0) {
+        e = launch_k3_pass<KeyT, PERM, kL3Threads>(p, ws, L, out_keys, out_perm, s, verify_fine, false, true, p.cap1,
+                                                   p.k3_smem1, std::min<int>(2 * num_sms(), (int)p.C));
+        if (e != cudaSuccess) return e;
+        return launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, verify_fine, true, false,
+                                                         p.cap, p.k3_smem, num_sms());
+    }
+    return launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, verify_fine, false, false,
+                                                     p.cap, p.k3_smem, std::min<int>(num_sms(), (int)p.C));
+}
+
+template <typename KeyT, bool PERM>
+cudaError_t launch_k3(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s,
+                      bool verify_fine) {
+    if (p.local) return launch_k3_local<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, verify_fine);
     switch (p.R) {
         case 1: return launch_k3_t<KeyT, PERM, 1>(p, ws, L, out_keys, out_perm, s);
         case 2: return launch_k3_t<KeyT, PERM, 2>(p, ws, L, out_keys, out_perm, s);
@@ -575,7 +615,8 @@ struct PhaseTimer {
 template <typename KeyT, bool PERM, bool GIVEN>
 int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int pred, KeyT* out_keys,
                  uint32_t* out_perm, void* ws, uint64_t ws_bytes, cudaStream_t s, mlsort_info* info,
-                 const uint32_t* bucket_in, const uint32_t* idx_in, uint32_t b_lo, bool timing = false) {
+                 const uint32_t* bucket_in, const uint32_t* idx_in, uint32_t b_lo, bool timing = false,
+                 bool verify_all = false) {
     Launches nl;
     PhaseTimer tm;
     const Plan p = make_plan(n, B, sizeof(KeyT), PERM, !GIVEN);
@@ -615,7 +656,13 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     k2_coarse_starts<<<1, 1024, 0, s>>>(at<uint32_t>(ws, L.cursor), p.C, at<unsigned long long>(ws, L.starts));
     CK(cudaGetLastError());
     tm.mark();
-    CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s)));
+    // Rank-bucket-level verification (reading A14) is needed only when the network is not
+    // provably monotone: with Eq. 4's sign condition every step of the f32 predictor is a
+    // monotone IEEE operation, so consecutive rank buckets cannot
+    // invert; K5 still checks every coarse-bucket boundary.  Received records (multi-GPU) and
+    // opts->verify == 2 are always verified.
+    const bool verify_fine = GIVEN || verify_all || !monotone(*w);
+    CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, verify_fine)));
     tm.mark();
     k4_big_copy<KeyT, PERM><<<num_sms(), kK3Threads, 0, s>>>(
         p.capc, p.R, at<KeyT>(ws, L.reg_keys), PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
@@ -628,7 +675,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
     CK(cudaGetLastError());
     tm.mark();
-    nl.count += 5;
+    nl.count += (p.local && p.cap1 > 0) ? 6 : 5;
 
     DevStatus* hs = host_status();
     CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
@@ -751,17 +798,18 @@ extern "C" int mlsort_sort(const void* d_keys, const uint32_t* d_payload, uint64
     ws_bytes -= (aligned - wsp);
     const bool perm = d_out_perm != nullptr;
     const bool timing = o && o->timing;
+    const bool verify_all = o && o->verify == 2;
     int rc;
     if (dt == MLSORT_F32) {
         rc = perm ? run_pipeline<float, true, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, d_out_perm,
-                                                     ws, ws_bytes, s, info, nullptr, nullptr, 0, timing)
+                                                     ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all)
                   : run_pipeline<float, false, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, nullptr,
-                                                      ws, ws_bytes, s, info, nullptr, nullptr, 0, timing);
+                                                      ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all);
     } else {
         rc = perm ? run_pipeline<double, true, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
-                                                      d_out_perm, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing)
+                                                      d_out_perm, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all)
                   : run_pipeline<double, false, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
-                                                       nullptr, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing);
+                                                       nullptr, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all);
     }
     if (rc == MLSORT_OK && d_out_payload) {
         k_gather_payload<float><<<grid_for(n, 256), 256, 0, s>>>(d_out_perm, d_payload, d_out_payload, n);
@@ -833,7 +881,7 @@ k_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Params 
             if (!KeyTraits<KeyT>::finite(x)) x = (KeyT)p.lo_d;
             key_to_u<KeyT>(x, p, u[q], ul[q]);
         }
-        gvm_forward_fxp<MPAD, PRED, G, false>(fw, u, ul, y);
+        gvm_forward_fxp<MPAD, PRED, G>(fw, u, ul, y);
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             const uint64_t i = i0 + (uint64_t)q * stride;

@@ -26,6 +26,9 @@ struct __align__(16) FoldedWeights {
     float C[kMaxM];
     float W[kMaxM];    // w2_j * 2^S (fixed-point accumulation scale, see below)
     float Wn[kMaxM];   // -W_j (the packed predictor carries -1/d)
+    // u in [u_safe_lo, u_safe_hi] keeps every argument a_j = A_j u + C_j <= 59, so the packed
+    // predictor may skip its per-activation clamp for such keys (CLAMP = false)
+    float u_safe_lo, u_safe_hi, pad_f[2];
     // (c, c) pairs of the packed predictor's constants, read from the parameter bank (uniform
     // registers) instead of occupying vector register pairs: 1, k1, 1.5*2^23
     unsigned long long one2, k1_2, magic2, pad2;
@@ -116,7 +119,9 @@ constexpr int32_t kFxpMagicBits = 0x4B400000;
 // MPAD is the padded neuron count (pad neurons have W = 0).  PRED selects the reciprocal
 // formulation; in kPredMixed one neuron in four uses MUFU.RCP and three use the Newton
 // reciprocal, balancing MUFU (ex2) load against FMA-pipe issue.
-template <int MPAD, int PRED, int KG, bool SPLIT>
+// CLAMP = false is valid only when every key of the group has u in [u_safe_lo, u_safe_hi]
+// (then a_j <= 59 for every neuron and d = 1 + 2^a is finite without the clamp).
+template <int MPAD, int PRED, int KG, bool CLAMP = true>
 __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const float (&uh)[KG],
                                                 const float (&ul)[KG], int32_t (&acc)[KG]) {
 #pragma unroll
@@ -130,12 +135,13 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
         for (int j = 0; j < MPAD / 2; ++j) {
 #pragma unroll
             for (int q = 0; q < KG; ++q) {
-                f32x2 a2 = ffma2(pk2(uh[q], uh[q]), A2[j], C2[j]);
-                if (SPLIT) a2 = ffma2(pk2(ul[q], ul[q]), A2[j], a2);
+                const f32x2 a2 = ffma2(pk2(uh[q], uh[q]), A2[j], C2[j]);
                 float a0, a1;
                 upk2(a2, a0, a1);
-                a0 = fminf(a0, 60.0f);               // d = 1 + 2^a stays finite and normal
-                a1 = fminf(a1, 60.0f);
+                if (CLAMP) {
+                    a0 = fminf(a0, 60.0f);           // d = 1 + 2^a stays finite and normal
+                    a1 = fminf(a1, 60.0f);
+                }
                 const f32x2 d2 = fadd2(pk2(ex2_approx(a0), ex2_approx(a1)), fw.one2);   // d = 1 + e
                 float d0, d1;
                 upk2(d2, d0, d1);
@@ -162,7 +168,6 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
 #pragma unroll
             for (int q = 0; q < KG; ++q) {
                 float a = fmaf(A, uh[q], C);
-                if (SPLIT) a = fmaf(A, ul[q], a);    // f64 keys: u = uh + ul carries 48 bits of u
                 float r;
                 if (use_mufu_rcp) {
                     r = rcp_approx(1.0f + ex2_approx(a));

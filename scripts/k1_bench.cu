@@ -6,6 +6,7 @@
 #include <cstring>
 #include <cmath>
 #include <vector>
+#include <algorithm>
 
 #include "../paper_1805_04272_b200/csrc/common.cuh"
 #include "../paper_1805_04272_b200/csrc/predict.cuh"
@@ -74,6 +75,15 @@ int main() {
         fw.Wn[j] = -fw.W[j];
     }
     auto pair = [](float v) { uint32_t b; std::memcpy(&b, &v, 4); return ((unsigned long long)b << 32) | b; };
+    double ulo = -INFINITY, uhi = INFINITY;
+    for (uint32_t j = 0; j < M; ++j) {
+        const double A = fw.A[j], Cc = fw.C[j];
+        if (A < 0) ulo = std::max(ulo, (59.0 - Cc) / A);
+        else if (A > 0) uhi = std::min(uhi, (59.0 - Cc) / A);
+    }
+    fw.u_safe_lo = (float)ulo + 1e-3f;
+    fw.u_safe_hi = uhi == INFINITY ? INFINITY : (float)uhi;
+    printf("safe u range [%g, %g]\n", fw.u_safe_lo, fw.u_safe_hi);
     fw.one2 = pair(1.0f);
     fw.k1_2 = pair(2.001281198f);
     fw.magic2 = pair(12582912.0f);
