@@ -6,11 +6,10 @@
 // both concurrently on different warps instead of alternating phases:
 //   * predictor warps (kPredWarps) evaluate the GVM for tile k into bucket buffer sb[k & 1];
 //   * partition warps (kPartWarps) take the previous tile from the other buffer: coarse-id
-//     histogram with shared atomics whose return value is every element's rank inside its
-//     (tile, coarse bucket) piece, one global reservation atomic per non-empty coarse bucket,
-//     and a direct store of every element to region slot = piece start + rank (keys, fine
-//     ids, input indices) -- the same output contract as k1_predict_partition (regions
-//     contiguous per coarse bucket, cursors = exact sizes).  No scan and no staging copy.
+//     histogram (shared atomics), scan, one global reservation atomic per non-empty coarse
+//     bucket, stable-by-position staging, and the store of every piece into its coarse
+//     bucket's region (keys, fine ids, input indices) -- the same output contract as
+//     k1_predict_partition (regions contiguous per coarse bucket, cursors = exact sizes).
 // The handoff is a double buffer guarded by named barriers (FULL[i]: predictors -> partition,
 // EMPTY[i]: partition -> predictors), so the SFU never waits for the partition.
 #pragma once
@@ -34,12 +33,11 @@ template <> struct WsTile<double> { static constexpr int kKeysPerThread = 8; };
 template <typename KeyT>
 __host__ __device__ constexpr int ws_tile() { return kPredThreads * WsTile<KeyT>::kKeysPerThread; }
 
-// smem: sb[2][T] u32 | hist[C'] u32 | gbase[C'] i64 | srank[T] u16
+// smem: sb[2][T] u32 | stage_key[T] KeyT | hist[C'] u32 | gbase[C'] i64 | stage_e[T] u16 | scratch
 // (C' = C rounded up to even so gbase is 8-B aligned)
 __host__ __device__ inline uint32_t k1ws_c2(uint32_t num_coarse) { return (num_coarse + 1u) & ~1u; }
 inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse) {
-    (void)ks;
-    return (size_t)tile * 8 + (size_t)k1ws_c2(num_coarse) * 12 + (size_t)tile * 2 + 256;
+    return (size_t)tile * 8 + (size_t)tile * ks + (size_t)k1ws_c2(num_coarse) * 12 + (size_t)tile * 2 + 256;
 }
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -58,10 +56,13 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
     enum { kFull0 = 1, kEmpty0 = 3, kPart = 5 };
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* sb = reinterpret_cast<uint32_t*>(smem);                         // [2][T]
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (size_t)T * 8);
+    KeyT* stage_key = reinterpret_cast<KeyT*>(smem + (size_t)T * 8);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (size_t)T * 8 + (size_t)T * sizeof(KeyT));
     const uint32_t C = p.num_coarse;
-    long long* gbase = reinterpret_cast<long long*>(hist + k1ws_c2(C));   // region slot of the piece start
-    uint16_t* srank = reinterpret_cast<uint16_t*>(gbase + k1ws_c2(C));     // rank inside the piece
+    long long* gbase = reinterpret_cast<long long*>(hist + k1ws_c2(C));   // region slot of position 0
+    uint16_t* stage_e = reinterpret_cast<uint16_t*>(gbase + k1ws_c2(C));
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(
+        (reinterpret_cast<uintptr_t>(stage_e + T) + 15) & ~(uintptr_t)15);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -145,9 +146,9 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
 
     // ===================================================== partition warps
     const int pt = tid - kPredThreads;                 // 0 .. kPartThreads-1
+    const int pw = warp - kPredWarps;
     const uint32_t fbits = p.fine_bits;
     const uint32_t fmask = (1u << fbits) - 1u;
-    const long long trash = (long long)C * p.capc;
     bool over = false;
     for (uint32_t k = 0; k < my_tiles; ++k) {
         const uint32_t tile = blockIdx.x + k * gridDim.x;
@@ -161,36 +162,70 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
             if (k + 2 < my_tiles) nbar_arrive(kEmpty0 + buf, kWsThreads);
             continue;
         }
-        // ---- coarse histogram; the atomic's return value is the element's rank in its piece
+        // ---- coarse histogram
 #pragma unroll 4
-        for (uint32_t e = pt; e < cnt; e += kPartThreads)
-            srank[e] = (uint16_t)atomicAdd(&hist[sbb[e] >> fbits], 1u);
+        for (uint32_t e = pt; e < cnt; e += kPartThreads) atomicAdd(&hist[sbb[e] >> fbits], 1u);
         nbar_sync(kPart, kPartThreads);
-        // ---- reserve this tile's piece in every region (one global atomic per non-empty bucket);
-        // a piece that would overflow its region is redirected to the trash rows after the
-        // regions (the call then falls back to the conventional sort)
+        // ---- scan (warp rows, conflict-free) + reservation of this tile's piece in every region.
+        // gbase[c] = slot of the tile's staged position 0 in the flat region array, so a staged
+        // element at position pos goes to gbase[c] + pos.  A piece that would overflow its
+        // region is redirected to the trash rows after the regions (the call then falls back).
+        {
+            const uint32_t chunk = (C + kPartWarps - 1) / kPartWarps;
+            const uint32_t b0 = min(C, (uint32_t)pw * chunk), b1 = min(C, b0 + chunk);
+            const long long trash = (long long)C * p.capc;
+            uint32_t carry = 0;
 #pragma unroll 4
-        for (uint32_t c = pt; c < C; c += kPartThreads) {
-            const uint32_t v = hist[c];
-            if (v) {
-                const uint32_t g = atomicAdd(&cursor[c], v);
-                const bool fits = (unsigned long long)g + v <= p.capc;
-                over |= !fits;
-                gbase[c] = fits ? (long long)c * p.capc + g : trash;
+            for (uint32_t r = b0; r < b1; r += 32) {
+                const uint32_t c = r + lane;
+                const uint32_t v = c < b1 ? hist[c] : 0u;
+                const uint32_t g = v ? atomicAdd(&cursor[c], v) : 0u;
+                uint32_t x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t yy = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += yy;
+                }
+                const uint32_t ex = carry + x - v;             // exclusive within the warp's chunk
+                if (c < b1) {
+                    hist[c] = ex;
+                    const bool fits = (unsigned long long)g + v <= p.capc;
+                    over |= !fits;
+                    gbase[c] = (fits ? (long long)c * p.capc + g : trash) - (long long)ex;
+                }
+                carry += __shfl_sync(0xffffffffu, x, 31);
             }
+            if (lane == 0) scratch[pw] = carry;
+            nbar_sync(kPart, kPartThreads);
+            uint32_t add = 0;
+            for (int w = 0; w < pw; ++w) add += scratch[w];
+            if (add)
+                for (uint32_t c = b0 + lane; c < b1; c += 32) {
+                    hist[c] += add;
+                    gbase[c] -= (long long)add;
+                }
         }
         nbar_sync(kPart, kPartThreads);
-        // ---- store every element to its region slot (the key is re-read from L2, coalesced)
+        // ---- stage the tile partitioned by coarse id (position -> original offset e, key)
 #pragma unroll 4
         for (uint32_t e = pt; e < cnt; e += kPartThreads) {
+            const uint32_t pos = atomicAdd(&hist[sbb[e] >> fbits], 1u);
+            stage_e[pos] = (uint16_t)e;
+            stage_key[pos] = keys[base + e];                   // L2-resident re-read
+        }
+        nbar_sync(kPart, kPartThreads);
+        // ---- store every piece into its coarse bucket's region
+#pragma unroll 4
+        for (uint32_t pos = pt; pos < cnt; pos += kPartThreads) {
+            const uint32_t e = stage_e[pos];
             const uint32_t b = sbb[e];
-            const size_t dst = (size_t)(gbase[b >> fbits] + srank[e]);
-            reg_keys[dst] = keys[base + e];
+            const size_t dst = (size_t)(gbase[b >> fbits] + (long long)pos);
+            reg_keys[dst] = stage_key[pos];
             reg_fine[dst] = (uint16_t)(b & fmask);
             if (PERM) reg_idx[dst] = (uint32_t)(base + e);
         }
         if (k + 2 < my_tiles) nbar_arrive(kEmpty0 + buf, kWsThreads);   // sb[buf] may be refilled
-        nbar_sync(kPart, kPartThreads);                // srank / hist / gbase free for the next tile
+        nbar_sync(kPart, kPartThreads);                // stage_* / hist free for the next tile
     }
     if (over) atomicAdd(&st->region_overflow, 1ull);
 }

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -183,7 +184,11 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
     const uint32_t fb_min = lb > 14 ? lb - 14 : 0;   // C <= 16384
     // Local plan (preferred): the fewest coarse buckets such that one CTA holds a coarse bucket
     // of 2x the average size in shared memory next to its rank-bucket histogram.
+    // MLSORT_FINE_BITS=<fb> forces the rank-bucket bits of the local plan (experiments only)
+    const char* fb_env = std::getenv("MLSORT_FINE_BITS");
+    const int fb_force = fb_env ? std::atoi(fb_env) : -1;
     for (int fb = (int)fb_max; fb >= (int)fb_min; --fb) {
+        if (fb_force >= 0 && fb != fb_force) continue;
         const uint64_t C = (B + (1ull << fb) - 1) >> fb;
         const size_t k1 = k1_smem_bytes(ks, perm, p.tile, (uint32_t)C);
         const bool ws_fits = allow_ws && k1ws_smem_bytes(ks, ws_tile_of(ks), (uint32_t)C) <= kK1WsSmemMax;
