@@ -30,9 +30,11 @@ struct K1Params {
     BucketMap bm;
     uint32_t fine_bits;      // b = c * 2^fine_bits + fine
     uint32_t num_coarse;     // C
-    uint32_t num_tiles;      // T
+    uint32_t num_tiles;      // tiles processed by this launch
     uint32_t capc;           // region capacity (elements) of every coarse bucket
     uint64_t n;
+    uint32_t tile0;          // first tile of this launch (chunked launches overlap the H2D copy)
+    uint32_t pad0;
 };
 
 template <typename KeyT> __device__ __forceinline__ void key_to_u(KeyT x, const K1Params& p, float& uh, float& ul);
@@ -79,7 +81,7 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
 
     constexpr int kKeysPerThread = kTile / kThreads;
     const int tid = threadIdx.x;
-    const uint32_t tile = blockIdx.x;
+    const uint32_t tile = p.tile0 + blockIdx.x;
     const uint64_t base = (uint64_t)tile * kTile;
     const uint32_t cnt = (uint32_t)min((uint64_t)kTile, p.n - base);
 

@@ -33,19 +33,28 @@ template <> struct WsTile<double> { static constexpr int kKeysPerThread = 8; };
 template <typename KeyT>
 __host__ __device__ constexpr int ws_tile() { return kPredThreads * WsTile<KeyT>::kKeysPerThread; }
 
-// smem: sb[2][T] u32 | stage_key[T] KeyT | hist[C'] u32 | gbase[C'] i64 | stage_e[T] u16 | scratch
-// (C' = C rounded up to even so gbase is 8-B aligned)
-__host__ __device__ inline uint32_t k1ws_c2(uint32_t num_coarse) { return (num_coarse + 1u) & ~1u; }
+// smem: sb[2][T] u32 | stage_key[T] KeyT | hist[C'] u32 | goff[C'] i32 | stage_e[T] u16 |
+//       cls_e[T] u16 | chist[64] u32 | ccur[64] u32 | lut[2048] u8 | scratch
+// (C' = C rounded up to a multiple of 4 so every array stays 16-B aligned)
+constexpr int kClasses = 64;
+__host__ __device__ inline uint32_t k1ws_c2(uint32_t num_coarse) { return (num_coarse + 3u) & ~3u; }
 inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse) {
-    return (size_t)tile * 8 + (size_t)tile * ks + (size_t)k1ws_c2(num_coarse) * 12 + (size_t)tile * 2 + 256;
+    return (size_t)tile * 8 + (size_t)tile * ks + (size_t)k1ws_c2(num_coarse) * 8 + (size_t)tile * 4 +
+           kClasses * 8 + 2048 + 256;
 }
+constexpr int32_t kOverflowOff = INT32_MIN;   // goff marker of a piece that overflowed its region
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // KGW = keys evaluated together per predictor thread (ILP); PARTITION = false skips the
 // partition work (scripts/k1_bench.cu uses it to measure the predictor warps alone).
-template <typename KeyT, int MPAD, int PRED, bool PERM, int KGW = 8, bool PARTITION = true>
+// GROUP = true (packed predictor only): each tile is first grouped by a 64-class value proxy
+// so a warp's 256 keys span a narrow range and saturated neuron pairs are skipped
+// (gvm_forward_skip).  Measured on C2 (M = 32) it is slower than plain evaluation (the
+// grouping, the L2 gathers and the per-pair control cost more than the ~47 % of pairs it
+// skips), so it is off by default.
+template <typename KeyT, int MPAD, int PRED, bool PERM, int KGW = 8, bool PARTITION = true, bool GROUP = false>
 __global__ void __launch_bounds__(kWsThreads, 1)
 k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restrict__ reg_keys,
       uint16_t* __restrict__ reg_fine, uint32_t* __restrict__ reg_idx, uint32_t* __restrict__ cursor,
@@ -53,21 +62,165 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
     constexpr int T = ws_tile<KeyT>();
     constexpr int KPT = WsTile<KeyT>::kKeysPerThread;
     constexpr int kGroupWs = KGW;
-    enum { kFull0 = 1, kEmpty0 = 3, kPart = 5 };
+    enum { kFull0 = 1, kEmpty0 = 3, kPart = 5, kPred = 6 };
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* sb = reinterpret_cast<uint32_t*>(smem);                         // [2][T]
     KeyT* stage_key = reinterpret_cast<KeyT*>(smem + (size_t)T * 8);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (size_t)T * 8 + (size_t)T * sizeof(KeyT));
     const uint32_t C = p.num_coarse;
-    long long* gbase = reinterpret_cast<long long*>(hist + k1ws_c2(C));   // region slot of position 0
-    uint16_t* stage_e = reinterpret_cast<uint16_t*>(gbase + k1ws_c2(C));
-    uint32_t* scratch = reinterpret_cast<uint32_t*>(
-        (reinterpret_cast<uintptr_t>(stage_e + T) + 15) & ~(uintptr_t)15);
+    int32_t* goff = reinterpret_cast<int32_t*>(hist + k1ws_c2(C));   // slot of position 0, minus c*capc
+    uint16_t* stage_e = reinterpret_cast<uint16_t*>(goff + k1ws_c2(C));
+    uint16_t* cls_e = stage_e + T;                                          // tile offsets in class order
+    uint32_t* chist = reinterpret_cast<uint32_t*>(cls_e + T);
+    uint32_t* ccur = chist + kClasses;
+    unsigned char* lut = reinterpret_cast<unsigned char*>(ccur + kClasses);
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(lut + 2048);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const uint32_t ntiles = p.num_tiles;
     const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (GROUP) {
+        for (int i = tid; i < 2048 / 4; i += kWsThreads)
+            reinterpret_cast<uint32_t*>(lut)[i] = reinterpret_cast<const uint32_t*>(fw.lut)[i];
+        if (tid < kClasses) chist[tid] = 0u;
+        __syncthreads();
+    }
+
+    if (GROUP && warp < kPredWarps) {
+        // ===================================================== predictor warps (value-grouped)
+        // A: load the tile (coalesced), validate, tail counts, class = lut[ordbits(u) >> 21];
+        //    class histogram (shared atomics).   B: scan the 64 classes.   C: scatter the tile
+        //    offsets into class order (cls_e).   D: evaluate 256 keys per warp in class order
+        //    (gathered from L2) with saturated-pair skipping; b goes to sb[buf][e].
+        uint32_t tail_lo = 0, tail_hi = 0;
+        for (uint32_t k = 0; k < my_tiles; ++k) {
+            const uint32_t tile = p.tile0 + blockIdx.x + k * gridDim.x;
+            const uint64_t base = (uint64_t)tile * T;
+            const uint32_t cnt = (uint32_t)min((uint64_t)T, p.n - base);
+            const int buf = k & 1;
+            uint32_t cls4[KPT / 4];                              // 8-bit classes, 4 per word
+#pragma unroll
+            for (int i = 0; i < KPT / 4; ++i) cls4[i] = 0u;
+#pragma unroll
+            for (int g = 0; g < KPT / 8; ++g) {
+                KeyT xv[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t e = tid + kPredThreads * (g * 8 + q);
+                    xv[q] = e < cnt ? keys[base + e] : (KeyT)p.lo_d;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int i = g * 8 + q;
+                    const uint32_t e = tid + kPredThreads * i;
+                    KeyT x = xv[q];
+                    if (!KeyTraits<KeyT>::finite(x)) {
+                        atomicMin(&st->bad_index, (unsigned long long)(base + e));
+                        x = (KeyT)p.lo_d;
+                    }
+                    if (e < cnt) {
+                        if (sizeof(KeyT) == 4) {
+                            tail_lo += (float)x < p.lo_tf;
+                            tail_hi += (float)x > p.hi_tf;
+                        } else {
+                            tail_lo += (double)x < p.lo_d;
+                            tail_hi += (double)x > p.hi_d;
+                        }
+                    }
+                    float uh, ulo;
+                    key_to_u<KeyT>(x, p, uh, ulo);
+                    const uint32_t c = e < cnt ? (uint32_t)lut[f32_ordbits(uh) >> 21] : (uint32_t)kClasses;
+                    cls4[i >> 2] |= c << ((i & 3) * 8);
+                    if (c < kClasses) atomicAdd(&chist[c], 1u);
+                }
+            }
+            nbar_sync(kPred, kPredThreads);
+            if (warp == 0) {                                     // B: exclusive scan of 64 classes
+                const uint32_t v0 = chist[2 * lane], v1 = chist[2 * lane + 1];
+                uint32_t x = v0 + v1;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t yy = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += yy;
+                }
+                const uint32_t ex = x - v0 - v1;
+                ccur[2 * lane] = ex;
+                ccur[2 * lane + 1] = ex + v0;
+                chist[2 * lane] = 0u;
+                chist[2 * lane + 1] = 0u;
+            }
+            nbar_sync(kPred, kPredThreads);
+#pragma unroll
+            for (int i = 0; i < KPT; ++i) {                      // C: scatter offsets in class order
+                const uint32_t e = tid + kPredThreads * i;
+                const uint32_t c = (cls4[i >> 2] >> ((i & 3) * 8)) & 0xffu;
+                if (c < kClasses) cls_e[atomicAdd(&ccur[c], 1u)] = (uint16_t)e;
+            }
+            nbar_sync(kPred, kPredThreads);
+            if (k >= 2) nbar_sync(kEmpty0 + buf, kWsThreads);    // partition released sb[buf]
+            uint32_t* sbb = sb + buf * T;
+            // D: this warp evaluates positions [w*KPT*32, (w+1)*KPT*32) of the class order
+            constexpr int GD = KPT / kGroupWs;
+            KeyT xn[kGroupWs];
+            uint32_t en[kGroupWs];
+            auto gather = [&](int g) {
+#pragma unroll
+                for (int q = 0; q < kGroupWs; ++q) {
+                    const uint32_t pos = (uint32_t)warp * (KPT * 32) + (g * kGroupWs + q) * 32 + lane;
+                    en[q] = pos < cnt ? (uint32_t)cls_e[pos] : 0xffffffffu;
+                    xn[q] = pos < cnt ? keys[base + en[q]] : (KeyT)p.lo_d;
+                }
+            };
+            gather(0);
+#pragma unroll 1
+            for (int g = 0; g < GD; ++g) {
+                KeyT xc[kGroupWs];
+                uint32_t ec[kGroupWs];
+#pragma unroll
+                for (int q = 0; q < kGroupWs; ++q) {
+                    xc[q] = xn[q];
+                    ec[q] = en[q];
+                }
+                if (g + 1 < GD) gather(g + 1);
+                float u[kGroupWs], ul[kGroupWs];
+                int32_t y[kGroupWs];
+                float mn = INFINITY, mx = -INFINITY;
+                bool safe = true;
+#pragma unroll
+                for (int q = 0; q < kGroupWs; ++q) {
+                    KeyT x = xc[q];
+                    if (!KeyTraits<KeyT>::finite(x)) x = (KeyT)p.lo_d;
+                    key_to_u<KeyT>(x, p, u[q], ul[q]);
+                    if (ec[q] != 0xffffffffu) {
+                        mn = fminf(mn, u[q]);
+                        mx = fmaxf(mx, u[q]);
+                    }
+                    safe &= (u[q] >= fw.u_safe_lo) & (u[q] <= fw.u_safe_hi);
+                }
+                // warp-wide range of u (order-preserving bits; empty lanes contribute nothing)
+                const uint32_t omn = __reduce_min_sync(0xffffffffu, f32_ordbits(mn));
+                const uint32_t omx = __reduce_max_sync(0xffffffffu, f32_ordbits(mx));
+                const float umin = __uint_as_float((omn & 0x80000000u) ? (omn & 0x7fffffffu) : ~omn);
+                const float umax = __uint_as_float((omx & 0x80000000u) ? (omx & 0x7fffffffu) : ~omx);
+                if (__all_sync(0xffffffffu, safe))
+                    gvm_forward_skip<MPAD, kGroupWs, false>(fw, u, umin, umax, y);
+                else
+                    gvm_forward_skip<MPAD, kGroupWs, true>(fw, u, umin, umax, y);
+#pragma unroll
+                for (int q = 0; q < kGroupWs; ++q)
+                    if (ec[q] != 0xffffffffu) sbb[ec[q]] = bucket_of_fxp(y[q], p.bm);
+            }
+            nbar_arrive(kFull0 + buf, kWsThreads);               // sb[buf] is ready
+        }
+        tail_lo = __reduce_add_sync(0xffffffffu, tail_lo);
+        tail_hi = __reduce_add_sync(0xffffffffu, tail_hi);
+        if (lane == 0) {
+            if (tail_lo) atomicAdd(&st->tail_lo, (unsigned long long)tail_lo);
+            if (tail_hi) atomicAdd(&st->tail_hi, (unsigned long long)tail_hi);
+        }
+        return;
+    }
 
     if (warp < kPredWarps) {
         // ===================================================== predictor warps
@@ -79,7 +232,7 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
         KeyT xn[kGroupWs];
         auto load_group = [&](uint32_t step) {
             const uint32_t k = step / G, g = step - k * G;
-            const uint64_t base = (uint64_t)(blockIdx.x + k * gridDim.x) * T;
+            const uint64_t base = (uint64_t)(p.tile0 + blockIdx.x + k * gridDim.x) * T;
             const uint32_t cnt = (uint32_t)min((uint64_t)T, p.n - base);
 #pragma unroll
             for (int q = 0; q < kGroupWs; ++q) {
@@ -91,7 +244,7 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
 #pragma unroll 1
         for (uint32_t step = 0; step < nsteps; ++step) {
             const uint32_t k = step / G, g = step - k * G;
-            const uint64_t base = (uint64_t)(blockIdx.x + k * gridDim.x) * T;
+            const uint64_t base = (uint64_t)(p.tile0 + blockIdx.x + k * gridDim.x) * T;
             const uint32_t cnt = (uint32_t)min((uint64_t)T, p.n - base);
             const int buf = k & 1;
             if (g == 0 && k >= 2) nbar_sync(kEmpty0 + buf, kWsThreads);   // partition released sb[buf]
@@ -151,7 +304,7 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
     const uint32_t fmask = (1u << fbits) - 1u;
     bool over = false;
     for (uint32_t k = 0; k < my_tiles; ++k) {
-        const uint32_t tile = blockIdx.x + k * gridDim.x;
+        const uint32_t tile = p.tile0 + blockIdx.x + k * gridDim.x;
         const uint64_t base = (uint64_t)tile * T;
         const uint32_t cnt = (uint32_t)min((uint64_t)T, p.n - base);
         const int buf = k & 1;
@@ -167,13 +320,12 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
         for (uint32_t e = pt; e < cnt; e += kPartThreads) atomicAdd(&hist[sbb[e] >> fbits], 1u);
         nbar_sync(kPart, kPartThreads);
         // ---- scan (warp rows, conflict-free) + reservation of this tile's piece in every region.
-        // gbase[c] = slot of the tile's staged position 0 in the flat region array, so a staged
-        // element at position pos goes to gbase[c] + pos.  A piece that would overflow its
-        // region is redirected to the trash rows after the regions (the call then falls back).
+        // goff[c] = slot of the tile's staged position 0 inside region c, so a staged element at
+        // position pos goes to c * capc + goff[c] + pos.  A piece that would overflow its region
+        // is marked kOverflowOff and not stored (the call then falls back to the conventional sort).
         {
             const uint32_t chunk = (C + kPartWarps - 1) / kPartWarps;
             const uint32_t b0 = min(C, (uint32_t)pw * chunk), b1 = min(C, b0 + chunk);
-            const long long trash = (long long)C * p.capc;
             uint32_t carry = 0;
 #pragma unroll 4
             for (uint32_t r = b0; r < b1; r += 32) {
@@ -191,7 +343,7 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
                     hist[c] = ex;
                     const bool fits = (unsigned long long)g + v <= p.capc;
                     over |= !fits;
-                    gbase[c] = (fits ? (long long)c * p.capc + g : trash) - (long long)ex;
+                    goff[c] = fits ? (int32_t)g - (int32_t)ex : kOverflowOff;
                 }
                 carry += __shfl_sync(0xffffffffu, x, 31);
             }
@@ -202,7 +354,7 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
             if (add)
                 for (uint32_t c = b0 + lane; c < b1; c += 32) {
                     hist[c] += add;
-                    gbase[c] -= (long long)add;
+                    if (goff[c] != kOverflowOff) goff[c] -= (int32_t)add;
                 }
         }
         nbar_sync(kPart, kPartThreads);
@@ -219,10 +371,14 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
         for (uint32_t pos = pt; pos < cnt; pos += kPartThreads) {
             const uint32_t e = stage_e[pos];
             const uint32_t b = sbb[e];
-            const size_t dst = (size_t)(gbase[b >> fbits] + (long long)pos);
-            reg_keys[dst] = stage_key[pos];
-            reg_fine[dst] = (uint16_t)(b & fmask);
-            if (PERM) reg_idx[dst] = (uint32_t)(base + e);
+            const uint32_t c = b >> fbits;
+            const int32_t off = goff[c];
+            if (off != kOverflowOff) {
+                const size_t dst = (size_t)c * p.capc + (size_t)(off + (int32_t)pos);
+                reg_keys[dst] = stage_key[pos];
+                reg_fine[dst] = (uint16_t)(b & fmask);
+                if (PERM) reg_idx[dst] = (uint32_t)(base + e);
+            }
         }
         if (k + 2 < my_tiles) nbar_arrive(kEmpty0 + buf, kWsThreads);   // sb[buf] may be refilled
         nbar_sync(kPart, kPartThreads);                // stage_* / hist free for the next tile

@@ -337,7 +337,11 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             const Bits kv = skey[pos];
             const uint32_t iv = PERM ? sidx[pos] : pos;
             uint32_t rank = 0;
+#if defined(MLSORT_K3L_EXPT) && MLSORT_K3L_EXPT == 2
+            if (false) {                       // experiment: no ranking
+#else
             if (len > 1) {
+#endif
                 if (len <= 4) {                // the common case: fixed, predicated compares
 #pragma unroll
                     for (uint32_t q = 0; q < 4; ++q) {
@@ -365,8 +369,12 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
                     continue;
                 }
             }
+#if defined(MLSORT_K3L_EXPT) && MLSORT_K3L_EXPT == 1
+            if (rank == 0xffffffffu) out_keys[S0] = KeyTraits<KeyT>::from_ord(kv);   // experiment: no store
+#else
             out_keys[S0 + s + rank] = KeyTraits<KeyT>::from_ord(kv);
             if (PERM) out_perm[S0 + s + rank] = iv;
+#endif
         }
         __syncthreads();
         K3L_T(4);

@@ -77,6 +77,25 @@ double origin_of(const Weights& w, bool f32) {
     return (double)(float)w.lo;
 }
 
+// Device reciprocal chain of the packed predictor evaluated at d = 1 (host emulation with IEEE
+// fma / multiply, bit-identical to FFMA2 / FMUL2): -r(1), the value every a <= -26 produces.
+float neg_rcp_at_one() {
+    auto bits_f = [](uint32_t b) { float f; std::memcpy(&f, &b, 4); return f; };
+    const float d = 1.0f, k1 = 2.001281198f;
+    const float nr0 = bits_f(0xFEF33400u - 0x3F800000u);
+    const float t = std::fmaf(d, nr0, k1);
+    const float nr1 = nr0 * t;
+    const float e = std::fmaf(d, nr1, 1.0f);
+    const float pp = std::fmaf(e, e, e);
+    return std::fmaf(nr1, pp, nr1);
+}
+
+uint32_t f32_bits(float v) {
+    uint32_t b;
+    std::memcpy(&b, &v, 4);
+    return b;
+}
+
 FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
     FoldedWeights f;
     std::memset(&f, 0, sizeof(f));
@@ -84,12 +103,24 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
     const double span = w.hi - w.lo;
     const double scale = std::ldexp(1.0, (int)fxp_shift(w));
     const double x0 = origin_of(w, f32);
+    // neurons sorted by the centre of their logistic (u where a_j = 0), so that the two neurons
+    // of a pair saturate together and a warp's narrow u range skips whole pairs; the sum of
+    // Eq. 3 is order-independent (exact integer accumulation)
+    std::vector<uint32_t> order(w.m);
+    for (uint32_t j = 0; j < w.m; ++j) order[j] = j;
+    auto centre = [&](uint32_t j) {
+        const double A = -2.0 * w.beta[j] * w.w1[j] * log2e / span;
+        const double C = w.beta[j] * (w.w1[j] + w.b[j]) * log2e + A * (x0 - w.lo);
+        return A != 0.0 ? -C / A : 0.0;
+    };
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return centre(a) < centre(b); });
     for (uint32_t j = 0; j < mpad; ++j) {
         if (j < w.m) {
-            const double A = -2.0 * w.beta[j] * w.w1[j] * log2e / span;
+            const uint32_t o = order[j];
+            const double A = -2.0 * w.beta[o] * w.w1[o] * log2e / span;
             f.A[j] = (float)A;
-            f.C[j] = (float)(w.beta[j] * (w.w1[j] + w.b[j]) * log2e + A * (x0 - w.lo));
-            f.W[j] = (float)(w.w2[j] * scale);
+            f.C[j] = (float)(w.beta[o] * (w.w1[o] + w.b[o]) * log2e + A * (x0 - w.lo));
+            f.W[j] = (float)(w.w2[o] * scale);
             f.Wn[j] = -f.W[j];
         } else {
             f.A[j] = 0.0f;
@@ -98,11 +129,75 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
             f.Wn[j] = 0.0f;
         }
     }
-    auto pair = [](float v) {
-        uint32_t b;
-        std::memcpy(&b, &v, 4);
-        return ((unsigned long long)b << 32) | b;
-    };
+    // ---- saturated-pair skipping bounds and constants (predict.cuh gvm_forward_skip)
+    const float nr_one = neg_rcp_at_one();
+    const uint32_t kMagicBits = 0x4B400000u;
+    for (uint32_t pp = 0; pp < mpad / 2; ++pp) {
+        double lo2 = INFINITY, hi2 = -INFINITY;
+        uint32_t tl = 0, tr = 0;
+        for (uint32_t h = 0; h < 2; ++h) {
+            const uint32_t j = 2 * pp + h;
+            const double A = f.A[j], C = f.C[j];
+            const uint32_t tzero = kMagicBits;
+            const uint32_t tsat = f32_bits(std::fmaf(nr_one, f.Wn[j], 12582912.0f));
+            double lo, hi;
+            uint32_t left, right;
+            if (A < 0) {            // u -> -inf: a -> +inf (term 0); u -> +inf: saturated
+                lo = (24.5 - C) / A;
+                hi = (-26.5 - C) / A;
+                left = tzero;
+                right = tsat;
+            } else if (A > 0) {     // u -> -inf: saturated; u -> +inf: term 0
+                lo = (-26.5 - C) / A;
+                hi = (24.5 - C) / A;
+                left = tsat;
+                right = tzero;
+            } else if (f.W[j] == 0.0f) {   // pad: a constant zero term everywhere
+                lo = INFINITY;
+                hi = -INFINITY;
+                left = right = tzero;
+            } else {                // a constant argument: never skipped
+                lo = -INFINITY;
+                hi = INFINITY;
+                left = right = tzero;
+            }
+            lo2 = std::min(lo2, lo);
+            hi2 = std::max(hi2, hi);
+            tl += left;
+            tr += right;
+        }
+        // round outwards so a skip decision on f32 u is always safe
+        float flo = (float)lo2, fhi = (float)hi2;
+        if (std::isfinite(flo) && (double)flo > lo2) flo = std::nextafter(flo, -INFINITY);
+        if (std::isfinite(fhi) && (double)fhi < hi2) fhi = std::nextafter(fhi, INFINITY);
+        f.lo2[pp] = flo;
+        f.hi2[pp] = fhi;
+        f.tl2[pp] = tl;
+        f.tr2[pp] = tr;
+    }
+    // ---- value classes for k1_ws's grouping: class = floor(64 y(u)) on a log-like grid of u
+    // (the top 11 order-preserving bits of the f32 u); only performance depends on it
+    for (uint32_t i = 0; i < 2048; ++i) {
+        const uint32_t ob = (i << 21) | (1u << 20);
+        const uint32_t bits = (ob & 0x80000000u) ? (ob & 0x7fffffffu) : ~ob;
+        float u;
+        std::memcpy(&u, &bits, 4);
+        int cls;
+        if (!std::isfinite(u)) {
+            cls = (ob & 0x80000000u) ? 63 : 0;
+        } else {
+            const double x = (double)u + x0;
+            const double xh = 2.0 * (x - w.lo) / span - 1.0;
+            double y = 0;
+            for (uint32_t j = 0; j < w.m; ++j) {
+                const double t = w.beta[j] * (w.w1[j] * xh - w.b[j]);
+                y += w.w2[j] / (1.0 + std::exp(-t));
+            }
+            cls = (int)std::floor(y * 64.0);
+            cls = std::max(0, std::min(63, cls));
+        }
+        f.lut[i] = (unsigned char)cls;
+    }
     // safe range of u for the clamp-free predictor: a_j = A_j u + C_j <= 59 for every neuron
     // (the f32 FFMA's rounding is far below the 59 -> 125 margin of the reciprocal chain)
     double ulo = -INFINITY, uhi = INFINITY;
@@ -115,11 +210,40 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
     f.u_safe_lo = ulo == -INFINITY ? -INFINITY : (float)std::nextafter((float)ulo, INFINITY);
     f.u_safe_hi = uhi == INFINITY ? INFINITY : (float)std::nextafter((float)uhi, -INFINITY);
     if (!(f.u_safe_lo <= f.u_safe_hi)) { f.u_safe_lo = INFINITY; f.u_safe_hi = -INFINITY; }
+    auto pair = [](float v) {
+        uint32_t bb;
+        std::memcpy(&bb, &v, 4);
+        return ((unsigned long long)bb << 32) | bb;
+    };
     f.one2 = pair(1.0f);
     f.k1_2 = pair(2.001281198f);
     f.magic2 = pair(12582912.0f);
     f.pad2 = 0;
     return f;
+}
+
+// Folding costs ~1 ms of host time (the 2048-entry class table evaluates the network); it is
+// done once per (weights handle, key dtype) and cached.
+const FoldedWeights& fold_cached(const Weights& w, uint32_t mpad, bool f32) {
+    struct Entry {
+        uint64_t serial;
+        uint32_t mpad;
+        bool f32;
+        FoldedWeights fw;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;     // small, most recent last
+    thread_local FoldedWeights result;
+    std::lock_guard<std::mutex> lock(mu);
+    for (size_t i = 0; i < cache.size(); ++i)
+        if (cache[i].serial == w.serial && cache[i].mpad == mpad && cache[i].f32 == f32) {
+            result = cache[i].fw;
+            return result;
+        }
+    if (cache.size() >= 16) cache.erase(cache.begin());
+    cache.push_back(Entry{w.serial, mpad, f32, fold(w, mpad, f32)});
+    result = cache.back().fw;
+    return result;
 }
 
 int pred_of(int32_t predictor) {
@@ -147,7 +271,7 @@ struct Plan {
 
 size_t k3_elem_bytes(size_t ks, bool perm) { return ks * 2 + 4 + (perm ? 8 : 0); }
 
-constexpr size_t kK1WsSmemMax = 231424;      // 226 KB
+constexpr size_t kK1WsSmemMax = 232448;      // 227 KB, the sm_100 per-block maximum
 
 uint32_t ws_tile_of(size_t ks) { return ks == 4 ? (uint32_t)ws_tile<float>() : (uint32_t)ws_tile<double>(); }
 
@@ -345,7 +469,7 @@ cudaError_t launch_k1_t(const Plan& p, const KeyT* keys, const FoldedWeights& fw
     auto kern = k1_predict_partition<KeyT, MPAD, PRED, PERM, GIVEN, kTileSmall>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k1_smem);
     if (e != cudaSuccess) return e;
-    kern<<<p.T, kThreads, p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
+    kern<<<kp.num_tiles, kThreads, p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
                                           PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
                                           at<uint32_t>(ws, L.cursor), at<DevStatus>(ws, L.status), bucket_in,
                                           idx_in, b_lo);
@@ -358,7 +482,7 @@ cudaError_t launch_k1_ws_t(const Plan& p, const KeyT* keys, const FoldedWeights&
     auto kern = k1_ws<KeyT, MPAD, PRED, PERM>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k1_smem);
     if (e != cudaSuccess) return e;
-    const int grid = std::min<int>(num_sms(), (int)p.T);
+    const int grid = std::min<int>(num_sms(), (int)kp.num_tiles);
     kern<<<grid, kWsThreads, p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
                                              PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr, at<uint32_t>(ws, L.cursor),
                                              at<DevStatus>(ws, L.status));
@@ -580,10 +704,20 @@ K1Params k1_params(const Weights& w, const Plan& p, uint64_t B, bool f32) {
     kp.fine_bits = p.fb;
     kp.num_coarse = p.C;
     kp.num_tiles = p.T;
+    kp.tile0 = 0;
+    kp.pad0 = 0;
     kp.capc = p.capc;
     kp.n = p.n;
     return kp;
 }
+
+// Chunked input arrival (mlsort_sort_host): K1 is launched per chunk of tiles after the chunk's
+// host-to-device copy has completed (event), so the copy of chunk i+1 overlaps K1 on chunk i.
+struct ChunkPlan {
+    int n = 0;
+    uint32_t tile_begin[16] = {}, tile_end[16] = {};
+    cudaEvent_t ready[16] = {};
+};
 
 // The core pipeline shared by mlsort_sort (predict) and mlsort_sort_records (GIVEN buckets).
 struct PhaseTimer {
@@ -621,7 +755,7 @@ template <typename KeyT, bool PERM, bool GIVEN>
 int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int pred, KeyT* out_keys,
                  uint32_t* out_perm, void* ws, uint64_t ws_bytes, cudaStream_t s, mlsort_info* info,
                  const uint32_t* bucket_in, const uint32_t* idx_in, uint32_t b_lo, bool timing = false,
-                 bool verify_all = false) {
+                 bool verify_all = false, const ChunkPlan* chunks = nullptr) {
     Launches nl;
     PhaseTimer tm;
     const Plan p = make_plan(n, B, sizeof(KeyT), PERM, !GIVEN);
@@ -643,7 +777,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     K1Params kp;
     if (!GIVEN) {
         mpad = mpad_of(w->m);
-        fw = fold(*w, mpad, sizeof(KeyT) == 4);
+        fw = fold_cached(*w, mpad, sizeof(KeyT) == 4);
         kp = k1_params(*w, p, B, sizeof(KeyT) == 4);
     } else {
         std::memset(&fw, 0, sizeof(fw));
@@ -656,7 +790,20 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     }
     if (pred != kPredMufu && pred != kPredMixed) pred = kPredPacked;
     tm.start(timing, s);
-    CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kp, ws, L, s, bucket_in, idx_in, b_lo)));
+    if (chunks && chunks->n > 0) {
+        for (int i = 0; i < chunks->n; ++i) {
+            CK(cudaStreamWaitEvent(s, chunks->ready[i], 0));
+            K1Params kc = kp;
+            kc.tile0 = chunks->tile_begin[i];
+            kc.num_tiles = chunks->tile_end[i] - chunks->tile_begin[i];
+            if (kc.num_tiles == 0) continue;
+            CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kc, ws, L, s, bucket_in, idx_in, b_lo)));
+            nl.count += 1;
+        }
+        nl.count -= 1;   // counted once below
+    } else {
+        CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kp, ws, L, s, bucket_in, idx_in, b_lo)));
+    }
     tm.mark();
     k2_coarse_starts<<<1, 1024, 0, s>>>(at<uint32_t>(ws, L.cursor), p.C, at<unsigned long long>(ws, L.starts));
     CK(cudaGetLastError());
@@ -776,9 +923,10 @@ extern "C" int mlsort_sort_workspace_size(uint64_t n, mlsort_dtype dt, const mls
     return MLSORT_OK;
 }
 
-extern "C" int mlsort_sort(const void* d_keys, const uint32_t* d_payload, uint64_t n, mlsort_dtype dt,
-                           const mlsort_weights* wh, const mlsort_opts* o, void* d_out_keys, uint32_t* d_out_perm,
-                           uint32_t* d_out_payload, void* d_ws, uint64_t ws_bytes, void* stream, mlsort_info* info) {
+namespace {
+int sort_impl(const void* d_keys, const uint32_t* d_payload, uint64_t n, mlsort_dtype dt, const mlsort_weights* wh,
+              const mlsort_opts* o, void* d_out_keys, uint32_t* d_out_perm, uint32_t* d_out_payload, void* d_ws,
+              uint64_t ws_bytes, void* stream, mlsort_info* info, const ChunkPlan* chunks) {
     if (info) {
         std::memset(info, 0, sizeof(*info));
         info->bad_index = -1;
@@ -807,14 +955,14 @@ extern "C" int mlsort_sort(const void* d_keys, const uint32_t* d_payload, uint64
     int rc;
     if (dt == MLSORT_F32) {
         rc = perm ? run_pipeline<float, true, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, d_out_perm,
-                                                     ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all)
+                                                     ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all, chunks)
                   : run_pipeline<float, false, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, nullptr,
-                                                      ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all);
+                                                      ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all, chunks);
     } else {
         rc = perm ? run_pipeline<double, true, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
-                                                      d_out_perm, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all)
+                                                      d_out_perm, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all, chunks)
                   : run_pipeline<double, false, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
-                                                       nullptr, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all);
+                                                       nullptr, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all, chunks);
     }
     if (rc == MLSORT_OK && d_out_payload) {
         k_gather_payload<float><<<grid_for(n, 256), 256, 0, s>>>(d_out_perm, d_payload, d_out_payload, n);
@@ -823,6 +971,14 @@ extern "C" int mlsort_sort(const void* d_keys, const uint32_t* d_payload, uint64
         if (info) info->kernel_launches += 1;
     }
     return rc;
+}
+}  // namespace
+
+extern "C" int mlsort_sort(const void* d_keys, const uint32_t* d_payload, uint64_t n, mlsort_dtype dt,
+                           const mlsort_weights* wh, const mlsort_opts* o, void* d_out_keys, uint32_t* d_out_perm,
+                           uint32_t* d_out_payload, void* d_ws, uint64_t ws_bytes, void* stream, mlsort_info* info) {
+    return sort_impl(d_keys, d_payload, n, dt, wh, o, d_out_keys, d_out_perm, d_out_payload, d_ws, ws_bytes, stream,
+                     info, nullptr);
 }
 
 extern "C" int mlsort_sort_host_workspace_size(uint64_t n, mlsort_dtype dt, const mlsort_opts* o, int want_perm,
@@ -859,8 +1015,42 @@ extern "C" int mlsort_sort_host(const void* h_keys, uint64_t n, mlsort_dtype dt,
     void* rest = base + need_io;
     const uint64_t rest_bytes = ws_bytes - (aligned - wsp) - need_io;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    CK(cudaMemcpyAsync(d_in, h_keys, n * ks, cudaMemcpyHostToDevice, s));
-    int rc = mlsort_sort(d_in, nullptr, n, dt, w, o, d_out, d_perm, nullptr, rest, rest_bytes, stream, info);
+    // The host-to-device copy is split into chunks of whole K1 tiles on a copy stream; K1 is
+    // launched per chunk as soon as that chunk has arrived, so prediction overlaps the copy.
+    thread_local cudaStream_t cs = nullptr;
+    thread_local cudaEvent_t evs[16] = {};
+    if (!cs) {
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (auto& e : evs) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const uint64_t B = (o && o->num_buckets) ? o->num_buckets : n;
+    ChunkPlan cp;
+    if (B <= (1ull << 30) && n < (1ull << 32)) {
+        const Plan pl = make_plan(n, B, ks, h_out_perm != nullptr, true);
+        const uint32_t nchunk = std::min<uint32_t>(8, pl.T);
+        const uint32_t per = (pl.T + nchunk - 1) / nchunk;
+        cudaEvent_t start_ev = evs[15];
+        CK(cudaEventRecord(start_ev, s));                 // the copy stream follows earlier work on s
+        CK(cudaStreamWaitEvent(cs, start_ev, 0));
+        for (uint32_t i = 0; i < nchunk; ++i) {
+            const uint32_t tb = i * per, te = std::min<uint32_t>(pl.T, tb + per);
+            if (tb >= te) break;
+            const uint64_t k0 = (uint64_t)tb * pl.tile, k1 = std::min<uint64_t>(n, (uint64_t)te * pl.tile);
+            CK(cudaMemcpyAsync(static_cast<char*>(d_in) + k0 * ks, static_cast<const char*>(h_keys) + k0 * ks,
+                               (k1 - k0) * ks, cudaMemcpyHostToDevice, cs));
+            CK(cudaEventRecord(evs[i], cs));
+            cp.tile_begin[cp.n] = tb;
+            cp.tile_end[cp.n] = te;
+            cp.ready[cp.n] = evs[i];
+            ++cp.n;
+        }
+        // (stream s waits on every chunk's event before that chunk's K1 launch, so everything
+        // after K1 -- K2..K5, fallbacks -- is ordered after the whole copy)
+    } else {
+        CK(cudaMemcpyAsync(d_in, h_keys, n * ks, cudaMemcpyHostToDevice, s));
+    }
+    int rc = sort_impl(d_in, nullptr, n, dt, w, o, d_out, d_perm, nullptr, rest, rest_bytes, stream, info,
+                       cp.n ? &cp : nullptr);
     if (rc) return rc;
     CK(cudaMemcpyAsync(h_out_keys, d_out, n * ks, cudaMemcpyDeviceToHost, s));
     if (h_out_perm) CK(cudaMemcpyAsync(h_out_perm, d_perm, n * 4, cudaMemcpyDeviceToHost, s));
@@ -902,7 +1092,7 @@ template <typename KeyT>
 int launch_predict(const KeyT* keys, uint64_t n, const Weights& w, uint64_t B, int pred, float* y, uint32_t* b,
                    cudaStream_t s) {
     const uint32_t mpad = mpad_of(w.m);
-    FoldedWeights fw = fold(w, mpad, sizeof(KeyT) == 4);
+    FoldedWeights fw = fold_cached(w, mpad, sizeof(KeyT) == 4);
     Plan p;
     p.n = n;
     K1Params kp = k1_params(w, p, B, sizeof(KeyT) == 4);
@@ -977,7 +1167,7 @@ extern "C" int mlsort_dist_partition(const void* d_shard, uint64_t n_local, uint
     init.bad_index = ~0ull;
     CK(cudaMemcpyAsync(dst, &init, sizeof(init), cudaMemcpyHostToDevice, s));
     const uint32_t mpad = mpad_of(w->m);
-    FoldedWeights fw = fold(*w, mpad, dt == MLSORT_F32);
+    FoldedWeights fw = fold_cached(*w, mpad, dt == MLSORT_F32);
     Plan p;
     p.n = n_local;
     K1Params kp = k1_params(*w, p, B, dt == MLSORT_F32);

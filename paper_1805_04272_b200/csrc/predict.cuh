@@ -29,6 +29,15 @@ struct __align__(16) FoldedWeights {
     // u in [u_safe_lo, u_safe_hi] keeps every argument a_j = A_j u + C_j <= 59, so the packed
     // predictor may skip its per-activation clamp for such keys (CLAMP = false)
     float u_safe_lo, u_safe_hi, pad_f[2];
+    // Saturated-pair skipping.  Neurons are stored sorted by
+    // centre.  For u < lo2[p] both neurons of pair p have a > 24.5 or a < -26.5 on their left
+    // side, and for u > hi2[p] on their right side; there the computed fixed-point terms are
+    // EXACT constants (a >= 24: |W r| < 1/4 rounds to 0; a <= -26: 1 + 2^a rounds to 1, so the
+    // reciprocal chain returns its value at d = 1), whose float bits are tl2[p] / tr2[p].
+    float lo2[kMaxM / 2], hi2[kMaxM / 2];
+    uint32_t tl2[kMaxM / 2], tr2[kMaxM / 2];
+    // class of a key for the value grouping in k1_ws: lut[ordered_bits(u) >> 21], 64 classes
+    unsigned char lut[2048];
     // (c, c) pairs of the packed predictor's constants, read from the parameter bank (uniform
     // registers) instead of occupying vector register pairs: 1, k1, 1.5*2^23
     unsigned long long one2, k1_2, magic2, pad2;
@@ -182,6 +191,64 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
         for (int q = 0; q < KG; ++q) acc[q] = (int32_t)((uint32_t)acc[q] + (uint32_t)t[0][q] + (uint32_t)t[1][q]);
     }
     }
+}
+
+// Packed predictor with saturated-pair skipping for a group of KG keys per lane whose u lie in
+// [umin, umax] across the warp (warp-uniform): a pair whose active interval misses
+// [umin, umax] contributes its exact constant bits; the others are evaluated.  The result is
+// bit-identical to gvm_forward_fxp<MPAD, kPredPacked, KG, CLAMP>.
+template <int MPAD, int KG, bool CLAMP>
+__device__ __forceinline__ void gvm_forward_skip(const FoldedWeights& fw, const float (&uh)[KG], float umin,
+                                                 float umax, int32_t (&acc)[KG]) {
+    uint32_t acc_c = 0u - (uint32_t)MPAD * (uint32_t)kFxpMagicBits;
+    uint32_t accv[KG];
+#pragma unroll
+    for (int q = 0; q < KG; ++q) accv[q] = 0u;
+    const f32x2* A2 = reinterpret_cast<const f32x2*>(fw.A);
+    const f32x2* C2 = reinterpret_cast<const f32x2*>(fw.C);
+    const f32x2* Wn2 = reinterpret_cast<const f32x2*>(fw.Wn);
+#pragma unroll 1
+    for (int j = 0; j < MPAD / 2; ++j) {
+        if (umax < fw.lo2[j]) {
+            acc_c += fw.tl2[j];
+            continue;
+        }
+        if (umin > fw.hi2[j]) {
+            acc_c += fw.tr2[j];
+            continue;
+        }
+        const f32x2 Aj = A2[j], Cj = C2[j], Wj = Wn2[j];
+#pragma unroll
+        for (int q = 0; q < KG; ++q) {
+            const f32x2 a2 = ffma2(pk2(uh[q], uh[q]), Aj, Cj);
+            float a0, a1;
+            upk2(a2, a0, a1);
+            if (CLAMP) {
+                a0 = fminf(a0, 60.0f);
+                a1 = fminf(a1, 60.0f);
+            }
+            const f32x2 d2 = fadd2(pk2(ex2_approx(a0), ex2_approx(a1)), fw.one2);
+            float d0, d1;
+            upk2(d2, d0, d1);
+            f32x2 nr2 = pk2(__uint_as_float(kSeedNeg - __float_as_uint(d0)),
+                            __uint_as_float(kSeedNeg - __float_as_uint(d1)));
+            nr2 = fmul2(nr2, ffma2(d2, nr2, fw.k1_2));
+            const f32x2 e2 = ffma2(d2, nr2, fw.one2);
+            nr2 = ffma2(nr2, ffma2(e2, e2, e2), nr2);
+            const f32x2 t2 = ffma2(nr2, Wj, fw.magic2);
+            float t0, t1;
+            upk2(t2, t0, t1);
+            accv[q] += __float_as_uint(t0) + __float_as_uint(t1);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < KG; ++q) acc[q] = (int32_t)(accv[q] + acc_c);
+}
+
+// order-preserving unsigned bits of an f32 (IEEE totalOrder)
+__device__ __forceinline__ uint32_t f32_ordbits(float x) {
+    const uint32_t u = __float_as_uint(x);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
 // r = clamp(round_half_up(y * B), 0, B - 1) with y = acc * 2^-S, in exact integer arithmetic

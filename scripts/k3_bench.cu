@@ -35,12 +35,13 @@ __global__ void gen_regions(float* rk, uint16_t* rf, const unsigned long long* s
 }
 
 int main() {
-    const uint32_t C = 4096, kfine = 16384, capc = 65600;
+    const uint32_t C = getenv("K3_FB13") ? 8192 : 4096, kfine = getenv("K3_FB13") ? 8192 : 16384;
+    const uint32_t capc = 4 * kfine + 64;
     std::vector<unsigned long long> starts(C + 1, 0);
     uint32_t s = 12345;
     for (uint32_t c = 0; c < C; ++c) {
         s = s * 1664525u + 1013904223u;
-        const uint32_t nc = 16384 - 256 + (s >> 23);     // 16128 .. 16639
+        const uint32_t nc = kfine - 256 + (s >> 23);     // kfine +- 256
         starts[c + 1] = starts[c] + nc;
     }
     const uint64_t n = starts[C];
