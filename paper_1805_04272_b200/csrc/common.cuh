@@ -25,8 +25,14 @@ struct DevStatus {
     unsigned long long local_repairs;   // coarse buckets re-sorted in K3 after an inversion
     unsigned long long mid_count;   // coarse buckets handed from the primary to the secondary K3 pass
     unsigned long long ticket3b;    // ticket of the secondary K3 pass
-    unsigned long long pad[2];
+    unsigned long long k3_violations;   // order violations found inside K3 slices (cluster K3)
+    unsigned long long pad[1];
 };
+
+// ---- start of coarse bucket c's region: c * capc, or the exact padded layout of a retry
+__device__ __forceinline__ size_t region_base(const unsigned long long* rbase, uint32_t c, uint32_t capc) {
+    return rbase ? (size_t)rbase[c] : (size_t)c * capc;
+}
 
 // ---- IEEE-754 totalOrder as unsigned integers (reading A10): negative -> ~bits,
 // non-negative -> bits | sign.  Equal order bits <=> bit-identical keys.

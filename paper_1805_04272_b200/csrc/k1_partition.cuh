@@ -67,7 +67,8 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
                      KeyT* __restrict__ reg_keys, uint16_t* __restrict__ reg_fine,
                      uint32_t* __restrict__ reg_idx, uint32_t* __restrict__ cursor,
                      DevStatus* __restrict__ st, const uint32_t* __restrict__ bucket_in = nullptr,
-                     const uint32_t* __restrict__ idx_in = nullptr, uint32_t b_lo = 0) {
+                     const uint32_t* __restrict__ idx_in = nullptr, uint32_t b_lo = 0,
+                     const unsigned long long* __restrict__ rbase = nullptr) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t C = p.num_coarse;
     // layout: stage_key[kTile] KeyT | stage_idx[kTile] u32 (PERM) | stage_b[kTile] u32 | hist[C] u32
@@ -201,8 +202,8 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
         const uint32_t b = stage_b[e];
         const uint32_t c = b >> p.fine_bits;
         const int32_t slot = gadj[c] + (int32_t)e;
-        if ((uint32_t)slot < p.capc) {
-            const size_t dst = (size_t)c * p.capc + (uint32_t)slot;
+        if (rbase || (uint32_t)slot < p.capc) {
+            const size_t dst = (rbase ? (size_t)rbase[c] : (size_t)c * p.capc) + (uint32_t)slot;
             reg_keys[dst] = stage_key[e];
             reg_fine[dst] = (uint16_t)(b & fmask);
             if (PERM) reg_idx[dst] = stage_idx[e];

@@ -14,35 +14,45 @@
 // EMPTY[i]: partition -> predictors), so the SFU never waits for the partition.
 #pragma once
 
+#include <climits>
+
 #include "common.cuh"
 #include "predict.cuh"
 #include "k1_partition.cuh"
 
 namespace mlsort {
 
-constexpr int kWsThreads = 1024;
-constexpr int kPredWarps = 24;
 constexpr int kPartWarps = 8;
-constexpr int kPredThreads = kPredWarps * 32;     // 768
 constexpr int kPartThreads = kPartWarps * 32;     // 256
+constexpr int kClasses = 64;
 
-template <typename KeyT> struct WsTile;
-template <> struct WsTile<float> { static constexpr int kKeysPerThread = 16; };
-template <> struct WsTile<double> { static constexpr int kKeysPerThread = 8; };
+// Warp split and tile of one k1_ws variant.  Plain: 24 predictor warps (1024 threads, 64
+// registers).  GROUP: 16 predictor warps (768 threads, up to 85 registers) and a smaller tile,
+// which leaves room for the tile's u values in class order.
+template <typename KeyT, bool GROUP>
+struct WsCfg {
+    static constexpr int kPredWarps = GROUP ? 16 : 24;
+    static constexpr int kThreads = (kPredWarps + kPartWarps) * 32;
+    static constexpr int kPredThreads = kPredWarps * 32;
+    static constexpr int kKPT = sizeof(KeyT) == 4 ? 16 : 8;   // keys per predictor thread per tile
+    static constexpr int kT = kPredThreads * kKPT;
+};
 
 template <typename KeyT>
-__host__ __device__ constexpr int ws_tile() { return kPredThreads * WsTile<KeyT>::kKeysPerThread; }
-
-// smem: sb[2][T] u32 | stage_key[T] KeyT | hist[C'] u32 | goff[C'] i32 | stage_e[T] u16 |
-//       cls_e[T] u16 | chist[64] u32 | ccur[64] u32 | lut[2048] u8 | scratch
-// (C' = C rounded up to a multiple of 4 so every array stays 16-B aligned)
-constexpr int kClasses = 64;
-__host__ __device__ inline uint32_t k1ws_c2(uint32_t num_coarse) { return (num_coarse + 3u) & ~3u; }
-inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse) {
-    return (size_t)tile * 8 + (size_t)tile * ks + (size_t)k1ws_c2(num_coarse) * 8 + (size_t)tile * 4 +
-           kClasses * 8 + 2048 + 256;
+__host__ __device__ constexpr int ws_tile(bool group = false) {
+    return group ? WsCfg<KeyT, true>::kT : WsCfg<KeyT, false>::kT;
 }
-constexpr int32_t kOverflowOff = INT32_MIN;   // goff marker of a piece that overflowed its region
+inline int ws_threads(bool group) { return group ? WsCfg<float, true>::kThreads : WsCfg<float, false>::kThreads; }
+
+// smem: sb[2][T] u32 | stage_key[T] KeyT | hist[C'] u32 | gbase[C'] i64 | stage_e[T] u16 |
+//       (GROUP: cls_u[T] f32 | cls_e[T] u16 | chist[64] | ccur[64] | lut[2048] u8) | scratch
+// (C' = C rounded up to a multiple of 4 so every array stays 16-B aligned)
+__host__ __device__ inline uint32_t k1ws_c2(uint32_t num_coarse) { return (num_coarse + 3u) & ~3u; }
+inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse, bool group = false) {
+    return (size_t)tile * 8 + (size_t)tile * ks + (size_t)k1ws_c2(num_coarse) * 12 + (size_t)tile * 2 +
+           (group ? (size_t)tile * 6 + kClasses * 8 + 2048 : 0) + 256;
+}
+constexpr long long kOverflowBase = LLONG_MIN;   // gbase marker of a piece that overflowed its region
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -51,16 +61,19 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.a
 // partition work (scripts/k1_bench.cu uses it to measure the predictor warps alone).
 // GROUP = true (packed predictor only): each tile is first grouped by a 64-class value proxy
 // so a warp's 256 keys span a narrow range and saturated neuron pairs are skipped
-// (gvm_forward_skip).  Measured on C2 (M = 32) it is slower than plain evaluation (the
-// grouping, the L2 gathers and the per-pair control cost more than the ~47 % of pairs it
-// skips), so it is off by default.
+// (gvm_forward_skip), with 16 predictor warps and the tile's u values kept in shared memory in
+// class order.
 template <typename KeyT, int MPAD, int PRED, bool PERM, int KGW = 8, bool PARTITION = true, bool GROUP = false>
-__global__ void __launch_bounds__(kWsThreads, 1)
+__global__ void __launch_bounds__(WsCfg<KeyT, GROUP>::kThreads, 1)
 k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restrict__ reg_keys,
       uint16_t* __restrict__ reg_fine, uint32_t* __restrict__ reg_idx, uint32_t* __restrict__ cursor,
-      DevStatus* __restrict__ st) {
-    constexpr int T = ws_tile<KeyT>();
-    constexpr int KPT = WsTile<KeyT>::kKeysPerThread;
+      DevStatus* __restrict__ st, const unsigned long long* __restrict__ rbase) {
+    using Cfg = WsCfg<KeyT, GROUP>;
+    constexpr int T = Cfg::kT;
+    constexpr int KPT = Cfg::kKPT;
+    constexpr int kPredWarps = Cfg::kPredWarps;
+    constexpr int kPredThreads = Cfg::kPredThreads;
+    constexpr int kWsThreads = Cfg::kThreads;
     constexpr int kGroupWs = KGW;
     enum { kFull0 = 1, kEmpty0 = 3, kPart = 5, kPred = 6 };
     extern __shared__ __align__(16) unsigned char smem[];
@@ -68,13 +81,14 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
     KeyT* stage_key = reinterpret_cast<KeyT*>(smem + (size_t)T * 8);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (size_t)T * 8 + (size_t)T * sizeof(KeyT));
     const uint32_t C = p.num_coarse;
-    int32_t* goff = reinterpret_cast<int32_t*>(hist + k1ws_c2(C));   // slot of position 0, minus c*capc
-    uint16_t* stage_e = reinterpret_cast<uint16_t*>(goff + k1ws_c2(C));
-    uint16_t* cls_e = stage_e + T;                                          // tile offsets in class order
-    uint32_t* chist = reinterpret_cast<uint32_t*>(cls_e + T);
-    uint32_t* ccur = chist + kClasses;
-    unsigned char* lut = reinterpret_cast<unsigned char*>(ccur + kClasses);
-    uint32_t* scratch = reinterpret_cast<uint32_t*>(lut + 2048);
+    long long* gbase = reinterpret_cast<long long*>(hist + k1ws_c2(C));   // region slot of staged position 0
+    uint16_t* stage_e = reinterpret_cast<uint16_t*>(gbase + k1ws_c2(C));
+    float* cls_u = reinterpret_cast<float*>(stage_e + T);                   // GROUP: u in class order
+    uint16_t* cls_e = reinterpret_cast<uint16_t*>(cls_u + (GROUP ? T : 0));  // GROUP: tile offsets
+    uint32_t* chist = reinterpret_cast<uint32_t*>(cls_e + (GROUP ? T : 0));
+    uint32_t* ccur = chist + (GROUP ? kClasses : 0);
+    unsigned char* lut = reinterpret_cast<unsigned char*>(ccur + (GROUP ? kClasses : 0));
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(lut + (GROUP ? 2048 : 0));
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -89,16 +103,17 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
 
     if (GROUP && warp < kPredWarps) {
         // ===================================================== predictor warps (value-grouped)
-        // A: load the tile (coalesced), validate, tail counts, class = lut[ordbits(u) >> 21];
-        //    class histogram (shared atomics).   B: scan the 64 classes.   C: scatter the tile
-        //    offsets into class order (cls_e).   D: evaluate 256 keys per warp in class order
-        //    (gathered from L2) with saturated-pair skipping; b goes to sb[buf][e].
+        // A: load the tile (coalesced), validate, tail counts, u, class = lut[ordbits(u) >> 21],
+        //    class histogram (shared atomics).   B: scan the 64 classes.   C: scatter (u, offset)
+        //    into class order.   D: each warp evaluates 512 consecutive keys of the class order
+        //    (two groups of 256: a narrow u range) with saturated-pair skipping; b -> sb[buf][e].
         uint32_t tail_lo = 0, tail_hi = 0;
         for (uint32_t k = 0; k < my_tiles; ++k) {
             const uint32_t tile = p.tile0 + blockIdx.x + k * gridDim.x;
             const uint64_t base = (uint64_t)tile * T;
             const uint32_t cnt = (uint32_t)min((uint64_t)T, p.n - base);
             const int buf = k & 1;
+            float ua[KPT];
             uint32_t cls4[KPT / 4];                              // 8-bit classes, 4 per word
 #pragma unroll
             for (int i = 0; i < KPT / 4; ++i) cls4[i] = 0u;
@@ -128,9 +143,9 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
                             tail_hi += (double)x > p.hi_d;
                         }
                     }
-                    float uh, ulo;
-                    key_to_u<KeyT>(x, p, uh, ulo);
-                    const uint32_t c = e < cnt ? (uint32_t)lut[f32_ordbits(uh) >> 21] : (uint32_t)kClasses;
+                    float ulo;
+                    key_to_u<KeyT>(x, p, ua[i], ulo);
+                    const uint32_t c = e < cnt ? (uint32_t)lut[f32_ordbits(ua[i]) >> 21] : (uint32_t)kClasses;
                     cls4[i >> 2] |= c << ((i & 3) * 8);
                     if (c < kClasses) atomicAdd(&chist[c], 1u);
                 }
@@ -152,47 +167,34 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
             }
             nbar_sync(kPred, kPredThreads);
 #pragma unroll
-            for (int i = 0; i < KPT; ++i) {                      // C: scatter offsets in class order
-                const uint32_t e = tid + kPredThreads * i;
+            for (int i = 0; i < KPT; ++i) {                      // C: scatter in class order
                 const uint32_t c = (cls4[i >> 2] >> ((i & 3) * 8)) & 0xffu;
-                if (c < kClasses) cls_e[atomicAdd(&ccur[c], 1u)] = (uint16_t)e;
+                if (c < kClasses) {
+                    const uint32_t pos = atomicAdd(&ccur[c], 1u);
+                    cls_u[pos] = ua[i];
+                    cls_e[pos] = (uint16_t)(tid + kPredThreads * i);
+                }
             }
             nbar_sync(kPred, kPredThreads);
             if (k >= 2) nbar_sync(kEmpty0 + buf, kWsThreads);    // partition released sb[buf]
             uint32_t* sbb = sb + buf * T;
             // D: this warp evaluates positions [w*KPT*32, (w+1)*KPT*32) of the class order
             constexpr int GD = KPT / kGroupWs;
-            KeyT xn[kGroupWs];
-            uint32_t en[kGroupWs];
-            auto gather = [&](int g) {
-#pragma unroll
-                for (int q = 0; q < kGroupWs; ++q) {
-                    const uint32_t pos = (uint32_t)warp * (KPT * 32) + (g * kGroupWs + q) * 32 + lane;
-                    en[q] = pos < cnt ? (uint32_t)cls_e[pos] : 0xffffffffu;
-                    xn[q] = pos < cnt ? keys[base + en[q]] : (KeyT)p.lo_d;
-                }
-            };
-            gather(0);
 #pragma unroll 1
             for (int g = 0; g < GD; ++g) {
-                KeyT xc[kGroupWs];
-                uint32_t ec[kGroupWs];
-#pragma unroll
-                for (int q = 0; q < kGroupWs; ++q) {
-                    xc[q] = xn[q];
-                    ec[q] = en[q];
-                }
-                if (g + 1 < GD) gather(g + 1);
                 float u[kGroupWs], ul[kGroupWs];
+                uint32_t ec[kGroupWs];
                 int32_t y[kGroupWs];
                 float mn = INFINITY, mx = -INFINITY;
                 bool safe = true;
 #pragma unroll
                 for (int q = 0; q < kGroupWs; ++q) {
-                    KeyT x = xc[q];
-                    if (!KeyTraits<KeyT>::finite(x)) x = (KeyT)p.lo_d;
-                    key_to_u<KeyT>(x, p, u[q], ul[q]);
-                    if (ec[q] != 0xffffffffu) {
+                    const uint32_t pos = (uint32_t)warp * (KPT * 32) + (g * kGroupWs + q) * 32 + lane;
+                    const bool valid = pos < cnt;
+                    u[q] = valid ? cls_u[pos] : 0.0f;
+                    ec[q] = valid ? (uint32_t)cls_e[pos] : 0xffffffffu;
+                    ul[q] = 0.0f;
+                    if (valid) {
                         mn = fminf(mn, u[q]);
                         mx = fmaxf(mx, u[q]);
                     }
@@ -320,9 +322,11 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
         for (uint32_t e = pt; e < cnt; e += kPartThreads) atomicAdd(&hist[sbb[e] >> fbits], 1u);
         nbar_sync(kPart, kPartThreads);
         // ---- scan (warp rows, conflict-free) + reservation of this tile's piece in every region.
-        // goff[c] = slot of the tile's staged position 0 inside region c, so a staged element at
-        // position pos goes to c * capc + goff[c] + pos.  A piece that would overflow its region
-        // is marked kOverflowOff and not stored (the call then falls back to the conventional sort).
+        // gbase[c] = region slot of the tile's staged position 0 for coarse bucket c, so a staged
+        // element at position pos goes to gbase[c] + pos.  Regions start at c * capc, or at
+        // rbase[c] (exact, padded sizes: the retry after an overflow).  A piece that would overflow
+        // its region is marked kOverflowBase and not stored; the call then retries with exact
+        // regions from the final cursors.
         {
             const uint32_t chunk = (C + kPartWarps - 1) / kPartWarps;
             const uint32_t b0 = min(C, (uint32_t)pw * chunk), b1 = min(C, b0 + chunk);
@@ -341,9 +345,10 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
                 const uint32_t ex = carry + x - v;             // exclusive within the warp's chunk
                 if (c < b1) {
                     hist[c] = ex;
-                    const bool fits = (unsigned long long)g + v <= p.capc;
+                    const bool fits = rbase != nullptr || (unsigned long long)g + v <= p.capc;
                     over |= !fits;
-                    goff[c] = fits ? (int32_t)g - (int32_t)ex : kOverflowOff;
+                    const long long rb = rbase ? (long long)rbase[c] : (long long)c * p.capc;
+                    gbase[c] = fits ? rb + (long long)g - (long long)ex : kOverflowBase;
                 }
                 carry += __shfl_sync(0xffffffffu, x, 31);
             }
@@ -354,7 +359,7 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
             if (add)
                 for (uint32_t c = b0 + lane; c < b1; c += 32) {
                     hist[c] += add;
-                    if (goff[c] != kOverflowOff) goff[c] -= (int32_t)add;
+                    if (gbase[c] != kOverflowBase) gbase[c] -= (long long)add;
                 }
         }
         nbar_sync(kPart, kPartThreads);
@@ -371,10 +376,9 @@ k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restr
         for (uint32_t pos = pt; pos < cnt; pos += kPartThreads) {
             const uint32_t e = stage_e[pos];
             const uint32_t b = sbb[e];
-            const uint32_t c = b >> fbits;
-            const int32_t off = goff[c];
-            if (off != kOverflowOff) {
-                const size_t dst = (size_t)c * p.capc + (size_t)(off + (int32_t)pos);
+            const long long gb = gbase[b >> fbits];
+            if (gb != kOverflowBase) {
+                const size_t dst = (size_t)(gb + (long long)pos);
                 reg_keys[dst] = stage_key[pos];
                 reg_fine[dst] = (uint16_t)(b & fmask);
                 if (PERM) reg_idx[dst] = (uint32_t)(base + e);

@@ -148,7 +148,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
               KeyT* __restrict__ out_keys, uint32_t* __restrict__ out_perm,
               unsigned long long* __restrict__ range_start, DevStatus* __restrict__ st,
               uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_mark, uint32_t* __restrict__ mid_list,
-              unsigned long long* __restrict__ ticket) {
+              unsigned long long* __restrict__ ticket, const unsigned long long* __restrict__ rbase) {
     using Bits = typename KeyTraits<KeyT>::Bits;
     extern __shared__ __align__(16) unsigned char smem[];
     // ctrl words: [1] next ticket, [2] big-queue count, [8..40) scan scratch,
@@ -172,7 +172,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         if (t0 < items) {
             const uint32_t c0 = coarse_of(t0);
             const unsigned long long s0 = starts[c0], n0 = starts[c0 + 1] - s0;
-            if (n0 <= p.cap) prefetch_bucket<KeyT, PERM>(reg_keys, reg_fine, reg_idx, (size_t)c0 * p.capc, n0);
+            if (n0 <= p.cap) prefetch_bucket<KeyT, PERM>(reg_keys, reg_fine, reg_idx, region_base(rbase, c0, p.capc), n0);
         }
     }
 #ifdef MLSORT_K3L_TIMING
@@ -195,7 +195,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             if (t1 < items) {
                 const uint32_t c1 = coarse_of(t1);
                 const unsigned long long s1 = starts[c1], n1 = starts[c1 + 1] - s1;
-                if (n1 <= p.cap) prefetch_bucket<KeyT, PERM>(reg_keys, reg_fine, reg_idx, (size_t)c1 * p.capc, n1);
+                if (n1 <= p.cap) prefetch_bucket<KeyT, PERM>(reg_keys, reg_fine, reg_idx, region_base(rbase, c1, p.capc), n1);
             }
         }
         if (n == 0) {
@@ -219,7 +219,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             range_start[c] = S0;
             atomicMax(&st->max_coarse, (unsigned long long)n);
         }
-        const size_t rb = (size_t)c * p.capc;
+        const size_t rb = region_base(rbase, c, p.capc);
         const KeyT* gk = reg_keys + rb;
         const uint16_t* gf = reg_fine + rb;
         const uint32_t* gi = PERM ? reg_idx + rb : nullptr;

@@ -140,7 +140,8 @@ k3_cluster_sort(K3Params p, const KeyT* __restrict__ reg_keys, const uint16_t* _
                 const uint32_t* __restrict__ reg_idx, const unsigned long long* __restrict__ starts,
                 KeyT* __restrict__ out_keys,
                 uint32_t* __restrict__ out_perm, unsigned long long* __restrict__ range_start,
-                DevStatus* __restrict__ st, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_mark) {
+                DevStatus* __restrict__ st, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_mark,
+                const unsigned long long* __restrict__ rbase) {
     static_assert(R <= 8, "owner counts are packed in 8-bit fields of one u64");
     using Bits = typename KeyTraits<KeyT>::Bits;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -189,7 +190,7 @@ k3_cluster_sort(K3Params p, const KeyT* __restrict__ reg_keys, const uint16_t* _
     // ---------------- phase A: stream this CTA's share of the region of c, route by owner
     const uint32_t e0 = (uint32_t)(((unsigned long long)r * n_c) / R);
     const uint32_t e1 = (uint32_t)(((unsigned long long)(r + 1) * n_c) / R);
-    const size_t rb0 = (size_t)c * p.capc;
+    const size_t rb0 = region_base(rbase, c, p.capc);
     const uint32_t fmask = p.kr - 1u;
     __syncthreads();                                   // local counters zeroed
     __cluster_barrier_wait();
@@ -352,7 +353,7 @@ k3_cluster_sort(K3Params p, const KeyT* __restrict__ reg_keys, const uint16_t* _
                 if (PERM) final_idx[i] = sorted_idx[i];
             }
         }
-        if (bigq[0] > kBigQ && tid == 0) atomicAdd(&st->violations, 1ull);   // not expected; forces repair
+        if (bigq[0] > kBigQ && tid == 0) atomicAdd(&st->k3_violations, 1ull);   // not expected; forces repair
     }
     __syncthreads();
     K3_STAMP(7);
@@ -372,7 +373,7 @@ k3_cluster_sort(K3Params p, const KeyT* __restrict__ reg_keys, const uint16_t* _
         if (PERM) out_perm[dst + e] = final_idx[e];
     }
     viol = __reduce_add_sync(0xffffffffu, viol);
-    if (lane == 0 && viol) atomicAdd(&st->violations, (unsigned long long)viol);
+    if (lane == 0 && viol) atomicAdd(&st->k3_violations, (unsigned long long)viol);
     K3_STAMP(8);
 }
 

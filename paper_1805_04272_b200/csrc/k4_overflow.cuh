@@ -28,7 +28,7 @@ k4_big_copy(uint32_t capc, uint32_t R, const KeyT* __restrict__ reg_keys, const 
             const unsigned long long* __restrict__ starts, KeyT* __restrict__ out_keys,
             uint32_t* __restrict__ out_perm, unsigned long long* __restrict__ range_start,
             DevStatus* __restrict__ st, const uint32_t* __restrict__ big_list, uint32_t* __restrict__ flags,
-            unsigned long long* __restrict__ ticket) {
+            unsigned long long* __restrict__ ticket, const unsigned long long* __restrict__ rbase) {
     using Bits = typename KeyTraits<KeyT>::Bits;
     __shared__ uint32_t s_k;
     __shared__ unsigned long long s_min, s_max;
@@ -46,7 +46,7 @@ k4_big_copy(uint32_t capc, uint32_t R, const KeyT* __restrict__ reg_keys, const 
         const uint32_t c = big_list[k];
         const unsigned long long S0 = starts[c], n_c = starts[c + 1] - S0;
         if (tid == 0) range_start[(size_t)c * R] = S0;
-        const size_t rb0 = (size_t)c * capc;
+        const size_t rb0 = region_base(rbase, c, capc);
         Bits vmin = ~(Bits)0, vmax = 0;
         for (unsigned long long i = tid; i < n_c; i += kK3Threads) {
             const KeyT key = reg_keys[rb0 + i];
@@ -128,6 +128,37 @@ k_radix_hist(const Bits* __restrict__ keys, const uint32_t* __restrict__ vals, u
     for (int d = threadIdx.x; d < 256; d += kRadixThreads) ghist[(size_t)d * nchunks + blockIdx.x] = h[d];
 }
 
+// Parallel in-place exclusive scan of m u32 entries: k_scan_blocks scans tiles of kScanTile
+// entries and records each tile's total, k_radix_scan (one CTA) scans the tile totals, and
+// k_scan_add adds every tile's offset.
+constexpr int kScanTile = 16384;
+__global__ void __launch_bounds__(1024) k_scan_blocks(uint32_t* __restrict__ a, uint64_t m, uint32_t* __restrict__ tot) {
+    __shared__ uint32_t scratch[64];
+    const uint64_t t0 = (uint64_t)blockIdx.x * kScanTile;
+    const uint64_t s = t0 + threadIdx.x * 16ull;
+    uint32_t v[16], local = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        v[i] = (s + i < m) ? a[s + i] : 0u;
+        local += v[i];
+    }
+    uint32_t total;
+    uint32_t run = block_exclusive_scan<1024>(local, scratch, &total);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        if (s + i < m) a[s + i] = run;
+        run += v[i];
+    }
+    if (threadIdx.x == 0) tot[blockIdx.x] = total;
+}
+__global__ void k_scan_add(uint32_t* __restrict__ a, uint64_t m, const uint32_t* __restrict__ tot) {
+    const uint32_t add = tot[blockIdx.x];
+    if (!add) return;
+    const uint64_t t0 = (uint64_t)blockIdx.x * kScanTile;
+    for (uint32_t i = threadIdx.x; i < kScanTile; i += blockDim.x)
+        if (t0 + i < m) a[t0 + i] += add;
+}
+
 // in-place exclusive scan of m entries with one CTA (digit-major order)
 __global__ void __launch_bounds__(1024) k_radix_scan(uint32_t* __restrict__ a, uint64_t m) {
     __shared__ uint32_t scratch[64];
@@ -201,6 +232,37 @@ k_radix_scatter(const Bits* __restrict__ kin, const uint32_t* __restrict__ vin, 
             const uint64_t dst = (uint64_t)goff[dig[r]] + wcnt[warp][dig[r]] + rank[r];
             kout[dst] = k[r];
             if (vout) vout[dst] = v[r];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ batched overflow sort
+// The overflow buckets are sorted together: their ranges are gathered into one contiguous
+// array (order-preserving key bits + index), that array is radix-sorted once, and the result is
+// scattered back range by range.  Valid because the network is monotone: every key of an
+// earlier coarse bucket precedes every key of a later one, so the sorted union splits into the
+// sorted buckets in order.
+template <typename KeyT>
+__global__ void k_seg_gather(const unsigned long long* __restrict__ seg, uint32_t nseg, const KeyT* __restrict__ keys,
+                             const uint32_t* __restrict__ perm, typename KeyTraits<KeyT>::Bits* __restrict__ tk,
+                             uint32_t* __restrict__ tv) {
+    for (uint32_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+        const unsigned long long src = seg[3 * g], dst = seg[3 * g + 1], len = seg[3 * g + 2];
+        for (unsigned long long i = threadIdx.x; i < len; i += blockDim.x) {
+            tk[dst + i] = KeyTraits<KeyT>::to_ord(keys[src + i]);
+            if (tv) tv[dst + i] = perm[src + i];
+        }
+    }
+}
+template <typename KeyT>
+__global__ void k_seg_scatter(const unsigned long long* __restrict__ seg, uint32_t nseg,
+                              const typename KeyTraits<KeyT>::Bits* __restrict__ tk, const uint32_t* __restrict__ tv,
+                              KeyT* __restrict__ keys, uint32_t* __restrict__ perm) {
+    for (uint32_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+        const unsigned long long src = seg[3 * g], dst = seg[3 * g + 1], len = seg[3 * g + 2];
+        for (unsigned long long i = threadIdx.x; i < len; i += blockDim.x) {
+            keys[src + i] = KeyTraits<KeyT>::from_ord(tk[dst + i]);
+            if (tv) perm[src + i] = tv[dst + i];
         }
     }
 }

@@ -266,6 +266,7 @@ struct Plan {
     uint32_t cap1 = 0;       // local plan: primary-pass capacity (two CTAs per SM)
     size_t k3_smem1 = 0;     // local plan: primary-pass shared memory
     bool ws = false;         // K1 = warp-specialized persistent k1_ws (tile = ws tile), else k1_predict_partition
+    bool ws_group = false;   // k1_ws with value grouping + saturated-pair skipping
     uint32_t kfine = 0;      // rank buckets per coarse bucket (local plan)
 };
 
@@ -273,19 +274,32 @@ size_t k3_elem_bytes(size_t ks, bool perm) { return ks * 2 + 4 + (perm ? 8 : 0);
 
 constexpr size_t kK1WsSmemMax = 232448;      // 227 KB, the sm_100 per-block maximum
 
-uint32_t ws_tile_of(size_t ks) { return ks == 4 ? (uint32_t)ws_tile<float>() : (uint32_t)ws_tile<double>(); }
+uint32_t ws_tile_of(size_t ks, bool group = false) {
+    return ks == 4 ? (uint32_t)ws_tile<float>(group) : (uint32_t)ws_tile<double>(group);
+}
+
+// K1 sparse evaluation (value grouping + saturated-pair skipping): packed predictor only;
+// MLSORT_GROUP=1 / 0 forces it on / off
+bool want_group(int pred, uint32_t mpad) {
+    if (pred != kPredPacked) return false;
+    const char* e = std::getenv("MLSORT_GROUP");
+    if (e) return std::atoi(e) != 0;
+    // measured on B200: M = 64 (C3) K1 14.9 -> 5.3 ms with grouping; M = 32 (C2) 1.01 -> 1.23 ms
+    return mpad >= 64;
+}
 
 Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws);
 
 // Choose the K1 variant after the coarse partition is fixed: the warp-specialized kernel when
 // its shared memory fits (and the caller predicts), else the phase-alternating one.
-Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws = true) {
+Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws = true, bool group = false) {
     Plan p = make_plan_base(n, B, ks, perm, allow_ws);
     if (allow_ws) {
-        const uint32_t wt = ws_tile_of(ks);
-        const size_t sm = k1ws_smem_bytes(ks, wt, p.C);
+        const uint32_t wt = ws_tile_of(ks, group);
+        const size_t sm = k1ws_smem_bytes(ks, wt, p.C, group);
         if (sm <= kK1WsSmemMax) {
             p.ws = true;
+            p.ws_group = group;
             p.tile = wt;
             p.T = (uint32_t)((n + wt - 1) / wt);
             p.k1_smem = sm;
@@ -364,7 +378,17 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
         }
     }
     if (!found) {   // heavily skewed sizes: smallest coarse buckets K1 allows, overflow path does the rest
-        p.fb = fb_min > 16 ? 16 : std::max<uint32_t>(fb_min, std::min<uint32_t>(fb_max, 16));
+        uint32_t fbc = std::min<uint32_t>(fb_max, 16);
+        for (int fb = (int)std::max(fb_min, 0u); fb <= (int)std::min<uint32_t>(fb_max, 16); ++fb) {
+            const uint64_t C = (B + (1ull << fb) - 1) >> fb;
+            const bool k1_ok = k1_smem_bytes(ks, perm, p.tile, (uint32_t)C) <= kK1SmemMax ||
+                               (allow_ws && k1ws_smem_bytes(ks, ws_tile_of(ks), (uint32_t)C) <= kK1WsSmemMax);
+            if (k1_ok) {
+                fbc = (uint32_t)fb;
+                break;
+            }
+        }
+        p.fb = fbc;
         p.C = (uint32_t)((B + (1ull << p.fb) - 1) >> p.fb);
         p.R = (1u << p.fb) >= 8 ? 8 : (1u << p.fb);
         p.kr = (1u << p.fb) / p.R;
@@ -384,13 +408,15 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
 // ---------------------------------------------------------------- workspace layout
 struct Layout {
     size_t status = 0, reg_keys = 0, reg_fine = 0, reg_idx = 0, cursor = 0, starts = 0,
-           range_start = 0, big_list = 0, flags = 0, big_mark = 0, radix = 0, mid_list = 0, total = 0;
+           range_start = 0, big_list = 0, flags = 0, big_mark = 0, radix = 0, mid_list = 0, segs = 0, rbase = 0,
+           total = 0;
     size_t radix_bytes = 0;
 };
 
 size_t radix_area(uint64_t n, size_t bits_bytes, bool payload) {
     const uint64_t nchunks = (n + kRadixChunk - 1) / kRadixChunk;
-    return align_up(n * bits_bytes) * 2 + (payload ? align_up(n * 4) * 2 : 0) + align_up(nchunks * 256 * 4);
+    return align_up(n * bits_bytes) * 2 + (payload ? align_up(n * 4) * 2 : 0) + align_up(nchunks * 256 * 4) +
+           align_up((nchunks * 256 / kScanTile + 1) * 4);
 }
 
 Layout make_layout(const Plan& p) {
@@ -421,6 +447,8 @@ Layout make_layout(const Plan& p) {
     L.flags = take((size_t)p.C * 4);
     L.big_mark = take((size_t)p.C * 4);
     L.mid_list = take((size_t)p.C * 4);
+    L.segs = take((size_t)p.C * 24);
+    L.rbase = take((size_t)p.C * 8);
     L.total = off;
     return L;
 }
@@ -465,41 +493,45 @@ struct Launches {
 template <typename KeyT, int MPAD, int PRED, bool PERM, bool GIVEN>
 cudaError_t launch_k1_t(const Plan& p, const KeyT* keys, const FoldedWeights& fw, const K1Params& kp,
                         void* ws, const Layout& L, cudaStream_t s, const uint32_t* bucket_in,
-                        const uint32_t* idx_in, uint32_t b_lo) {
+                        const uint32_t* idx_in, uint32_t b_lo, const unsigned long long* rbase) {
     auto kern = k1_predict_partition<KeyT, MPAD, PRED, PERM, GIVEN, kTileSmall>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k1_smem);
     if (e != cudaSuccess) return e;
     kern<<<kp.num_tiles, kThreads, p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
                                           PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
                                           at<uint32_t>(ws, L.cursor), at<DevStatus>(ws, L.status), bucket_in,
-                                          idx_in, b_lo);
+                                          idx_in, b_lo, rbase);
     return cudaGetLastError();
 }
 
 template <typename KeyT, int MPAD, int PRED, bool PERM>
 cudaError_t launch_k1_ws_t(const Plan& p, const KeyT* keys, const FoldedWeights& fw, const K1Params& kp, void* ws,
-                           const Layout& L, cudaStream_t s) {
-    auto kern = k1_ws<KeyT, MPAD, PRED, PERM>;
+                           const Layout& L, cudaStream_t s, const unsigned long long* rbase) {
+    const bool group = PRED == kPredPacked && p.ws_group;
+    auto kern = group ? k1_ws<KeyT, MPAD, PRED, PERM, 8, true, PRED == kPredPacked>
+                      : k1_ws<KeyT, MPAD, PRED, PERM, 8, true, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k1_smem);
     if (e != cudaSuccess) return e;
     const int grid = std::min<int>(num_sms(), (int)kp.num_tiles);
-    kern<<<grid, kWsThreads, p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
+    kern<<<grid, ws_threads(group), p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
                                              PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr, at<uint32_t>(ws, L.cursor),
-                                             at<DevStatus>(ws, L.status));
+                                             at<DevStatus>(ws, L.status), rbase);
     return cudaGetLastError();
 }
 
 template <typename KeyT, bool PERM, bool GIVEN>
 cudaError_t launch_k1(const Plan& p, const KeyT* keys, uint32_t mpad, int pred, const FoldedWeights& fw,
                       const K1Params& kp, void* ws, const Layout& L, cudaStream_t s,
-                      const uint32_t* bucket_in = nullptr, const uint32_t* idx_in = nullptr, uint32_t b_lo = 0) {
-    if (GIVEN) return launch_k1_t<KeyT, 16, kPredMufu, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo);
+                      const uint32_t* bucket_in = nullptr, const uint32_t* idx_in = nullptr, uint32_t b_lo = 0,
+                      const unsigned long long* rbase = nullptr) {
+    if (GIVEN)
+        return launch_k1_t<KeyT, 16, kPredMufu, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo, rbase);
     if (!GIVEN && p.ws) {
 #define K1WS(M)                                                                                            \
         if (mpad == M) {                                                                                   \
-            if (pred == kPredMufu) return launch_k1_ws_t<KeyT, M, kPredMufu, PERM>(p, keys, fw, kp, ws, L, s);   \
-            if (pred == kPredMixed) return launch_k1_ws_t<KeyT, M, kPredMixed, PERM>(p, keys, fw, kp, ws, L, s); \
-            return launch_k1_ws_t<KeyT, M, kPredPacked, PERM>(p, keys, fw, kp, ws, L, s);                   \
+            if (pred == kPredMufu) return launch_k1_ws_t<KeyT, M, kPredMufu, PERM>(p, keys, fw, kp, ws, L, s, rbase);   \
+            if (pred == kPredMixed) return launch_k1_ws_t<KeyT, M, kPredMixed, PERM>(p, keys, fw, kp, ws, L, s, rbase); \
+            return launch_k1_ws_t<KeyT, M, kPredPacked, PERM>(p, keys, fw, kp, ws, L, s, rbase);                   \
         }
         K1WS(16) K1WS(32) K1WS(64)
 #undef K1WS
@@ -508,10 +540,10 @@ cudaError_t launch_k1(const Plan& p, const KeyT* keys, uint32_t mpad, int pred, 
 #define K1CASE(M)                                                                                          \
     if (mpad == M) {                                                                                       \
         if (pred == kPredMufu)                                                                             \
-            return launch_k1_t<KeyT, M, kPredMufu, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo); \
+            return launch_k1_t<KeyT, M, kPredMufu, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo, rbase); \
         if (pred == kPredPacked)                                                                           \
-            return launch_k1_t<KeyT, M, kPredPacked, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo); \
-        return launch_k1_t<KeyT, M, kPredMixed, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo);    \
+            return launch_k1_t<KeyT, M, kPredPacked, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo, rbase); \
+        return launch_k1_t<KeyT, M, kPredMixed, PERM, GIVEN>(p, keys, fw, kp, ws, L, s, bucket_in, idx_in, b_lo, rbase);    \
     }
     K1CASE(16) K1CASE(32) K1CASE(64)
 #undef K1CASE
@@ -520,7 +552,7 @@ cudaError_t launch_k1(const Plan& p, const KeyT* keys, uint32_t mpad, int pred, 
 
 template <typename KeyT, bool PERM, int R>
 cudaError_t launch_k3_t(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm,
-                        cudaStream_t s) {
+                        cudaStream_t s, const unsigned long long* rbase) {
     auto kern = k3_cluster_sort<KeyT, PERM, R>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k3_smem);
     if (e != cudaSuccess) return e;
@@ -549,12 +581,13 @@ cudaError_t launch_k3_t(const Plan& p, void* ws, const Layout& L, KeyT* out_keys
                               (const uint32_t*)(PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr),
                               (const unsigned long long*)at<unsigned long long>(ws, L.starts), out_keys, out_perm,
                               at<unsigned long long>(ws, L.range_start), at<DevStatus>(ws, L.status),
-                              at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.big_mark));
+                              at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.big_mark), rbase);
 }
 
 template <typename KeyT, bool PERM, int NT>
 cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s,
-                           bool verify_fine, bool secondary, bool to_mid, uint32_t cap, size_t smem, int grid) {
+                           bool verify_fine, bool secondary, bool to_mid, uint32_t cap, size_t smem, int grid,
+                           const unsigned long long* rbase) {
     auto kern = k3_local_sort<KeyT, PERM, NT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -571,7 +604,7 @@ cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_k
                                 PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr, at<unsigned long long>(ws, L.starts),
                                 out_keys, out_perm, at<unsigned long long>(ws, L.range_start), st,
                                 at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.big_mark), at<uint32_t>(ws, L.mid_list),
-                                secondary ? &st->ticket3b : &st->ticket3);
+                                secondary ? &st->ticket3b : &st->ticket3, rbase);
     return cudaGetLastError();
 }
 
@@ -580,28 +613,28 @@ cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_k
 // the primary pass handed over.
 template <typename KeyT, bool PERM>
 cudaError_t launch_k3_local(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm,
-                            cudaStream_t s, bool verify_fine) {
+                            cudaStream_t s, bool verify_fine, const unsigned long long* rbase) {
     cudaError_t e;
     if (p.cap1 > 0) {
         e = launch_k3_pass<KeyT, PERM, kL3Threads>(p, ws, L, out_keys, out_perm, s, verify_fine, false, true, p.cap1,
-                                                   p.k3_smem1, std::min<int>(2 * num_sms(), (int)p.C));
+                                                   p.k3_smem1, std::min<int>(2 * num_sms(), (int)p.C), rbase);
         if (e != cudaSuccess) return e;
         return launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, verify_fine, true, false,
-                                                         p.cap, p.k3_smem, num_sms());
+                                                         p.cap, p.k3_smem, num_sms(), rbase);
     }
     return launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, verify_fine, false, false,
-                                                     p.cap, p.k3_smem, std::min<int>(num_sms(), (int)p.C));
+                                                     p.cap, p.k3_smem, std::min<int>(num_sms(), (int)p.C), rbase);
 }
 
 template <typename KeyT, bool PERM>
 cudaError_t launch_k3(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s,
-                      bool verify_fine) {
-    if (p.local) return launch_k3_local<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, verify_fine);
+                      bool verify_fine, const unsigned long long* rbase) {
+    if (p.local) return launch_k3_local<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, verify_fine, rbase);
     switch (p.R) {
-        case 1: return launch_k3_t<KeyT, PERM, 1>(p, ws, L, out_keys, out_perm, s);
-        case 2: return launch_k3_t<KeyT, PERM, 2>(p, ws, L, out_keys, out_perm, s);
-        case 4: return launch_k3_t<KeyT, PERM, 4>(p, ws, L, out_keys, out_perm, s);
-        case 8: return launch_k3_t<KeyT, PERM, 8>(p, ws, L, out_keys, out_perm, s);
+        case 1: return launch_k3_t<KeyT, PERM, 1>(p, ws, L, out_keys, out_perm, s, rbase);
+        case 2: return launch_k3_t<KeyT, PERM, 2>(p, ws, L, out_keys, out_perm, s, rbase);
+        case 4: return launch_k3_t<KeyT, PERM, 4>(p, ws, L, out_keys, out_perm, s, rbase);
+        case 8: return launch_k3_t<KeyT, PERM, 8>(p, ws, L, out_keys, out_perm, s, rbase);
         default: break;
     }
     return cudaErrorInvalidValue;
@@ -621,7 +654,19 @@ int radix_sort_pairs(Bits* k0, uint32_t* v0, Bits* k1, uint32_t* v1, uint32_t* g
         Bits* ko = cur ? k0 : k1;
         uint32_t* vo = cur ? v0 : v1;
         k_radix_hist<Bits><<<nchunks, kRadixThreads, 0, s>>>(ki, vi, n, field, shift, nchunks, ghist);
-        k_radix_scan<<<1, 1024, 0, s>>>(ghist, (uint64_t)nchunks * 256);
+        {   // digit-major exclusive scan of the chunk histograms
+            const uint64_t m = (uint64_t)nchunks * 256;
+            const uint32_t nt = (uint32_t)((m + kScanTile - 1) / kScanTile);
+            if (nt <= 1) {
+                k_radix_scan<<<1, 1024, 0, s>>>(ghist, m);
+            } else {
+                uint32_t* tot = ghist + m;                 // scratch after the histograms
+                k_scan_blocks<<<nt, 1024, 0, s>>>(ghist, m, tot);
+                k_radix_scan<<<1, 1024, 0, s>>>(tot, nt);
+                k_scan_add<<<nt, 256, 0, s>>>(ghist, m, tot);
+                nl.count += 2;
+            }
+        }
         k_radix_scatter<Bits><<<nchunks, kRadixThreads, 0, s>>>(ki, vi, ko, vo, n, field, shift, nchunks, ghist);
         nl.count += 3;
         cur ^= 1;
@@ -758,20 +803,11 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
                  bool verify_all = false, const ChunkPlan* chunks = nullptr) {
     Launches nl;
     PhaseTimer tm;
-    const Plan p = make_plan(n, B, sizeof(KeyT), PERM, !GIVEN);
+    const bool group = !GIVEN && want_group(pred == kPredMufu || pred == kPredMixed ? pred : kPredPacked,
+                                            GIVEN ? 16 : mpad_of(w->m));
+    const Plan p = make_plan(n, B, sizeof(KeyT), PERM, !GIVEN, group);
     const Layout L = make_layout(p);
     if (ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign)) return MLSORT_ERR_WORKSPACE;
-    DevStatus* dst = at<DevStatus>(ws, L.status);
-    {
-        DevStatus init;
-        std::memset(&init, 0, sizeof(init));
-        init.bad_index = ~0ull;
-        CK(cudaMemcpyAsync(dst, &init, sizeof(init), cudaMemcpyHostToDevice, s));
-    }
-    CK(cudaMemsetAsync(at<void>(ws, L.range_start), 0xff, (size_t)p.C * p.R * 8, s));
-    CK(cudaMemsetAsync(at<void>(ws, L.big_mark), 0, (size_t)p.C * 4, s));
-    CK(cudaMemsetAsync(at<void>(ws, L.cursor), 0, (size_t)p.C * 4, s));
-
     FoldedWeights fw;
     uint32_t mpad = 16;
     K1Params kp;
@@ -790,62 +826,98 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     }
     if (pred != kPredMufu && pred != kPredMixed) pred = kPredPacked;
     tm.start(timing, s);
-    if (chunks && chunks->n > 0) {
-        for (int i = 0; i < chunks->n; ++i) {
-            CK(cudaStreamWaitEvent(s, chunks->ready[i], 0));
-            K1Params kc = kp;
-            kc.tile0 = chunks->tile_begin[i];
-            kc.num_tiles = chunks->tile_end[i] - chunks->tile_begin[i];
-            if (kc.num_tiles == 0) continue;
-            CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kc, ws, L, s, bucket_in, idx_in, b_lo)));
-            nl.count += 1;
-        }
-        nl.count -= 1;   // counted once below
-    } else {
-        CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kp, ws, L, s, bucket_in, idx_in, b_lo)));
-    }
-    tm.mark();
-    k2_coarse_starts<<<1, 1024, 0, s>>>(at<uint32_t>(ws, L.cursor), p.C, at<unsigned long long>(ws, L.starts));
-    CK(cudaGetLastError());
-    tm.mark();
-    // Rank-bucket-level verification (reading A14) is needed only when the network is not
-    // provably monotone: with Eq. 4's sign condition every step of the f32 predictor is a
-    // monotone IEEE operation, so consecutive rank buckets cannot
-    // invert; K5 still checks every coarse-bucket boundary.  Received records (multi-GPU) and
-    // opts->verify == 2 are always verified.
-    const bool verify_fine = GIVEN || verify_all || !monotone(*w);
-    CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, verify_fine)));
-    tm.mark();
-    k4_big_copy<KeyT, PERM><<<num_sms(), kK3Threads, 0, s>>>(
-        p.capc, p.R, at<KeyT>(ws, L.reg_keys), PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
-        at<unsigned long long>(ws, L.starts), out_keys, out_perm, at<unsigned long long>(ws, L.range_start), dst,
-        at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.flags), &dst->ticket);
-    CK(cudaGetLastError());
-    tm.mark();
-    const uint64_t nranges = (uint64_t)p.C * p.R;
-    k5_boundary_verify<KeyT, PERM><<<(unsigned)((nranges + 255) / 256), 256, 0, s>>>(
-        at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
-    CK(cudaGetLastError());
-    tm.mark();
-    nl.count += (p.local && p.cap1 > 0) ? 6 : 5;
-
+    DevStatus* dst = at<DevStatus>(ws, L.status);
     DevStatus* hs = host_status();
-    CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    tm.finish(info);
-    DevStatus st = *hs;
-    if (info) {
-        info->num_coarse = p.C;
-        info->tail_lo = st.tail_lo;
-        info->tail_hi = st.tail_hi;
-        info->max_coarse = st.max_coarse;
-        info->big_buckets = st.big_count;
+    DevStatus st;
+    const unsigned long long* rbase = nullptr;   // regions at c * capc; exact layout on a retry
+    const uint64_t nranges = (uint64_t)p.C * p.R;
+    for (int attempt = 0;; ++attempt) {
+        {
+            DevStatus init;
+            std::memset(&init, 0, sizeof(init));
+            init.bad_index = ~0ull;
+            CK(cudaMemcpyAsync(dst, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+        }
+        CK(cudaMemsetAsync(at<void>(ws, L.range_start), 0xff, (size_t)p.C * p.R * 8, s));
+        CK(cudaMemsetAsync(at<void>(ws, L.big_mark), 0, (size_t)p.C * 4, s));
+        CK(cudaMemsetAsync(at<void>(ws, L.cursor), 0, (size_t)p.C * 4, s));
+
+        if (chunks && chunks->n > 0) {
+            for (int i = 0; i < chunks->n; ++i) {
+                CK(cudaStreamWaitEvent(s, chunks->ready[i], 0));
+                K1Params kc = kp;
+                kc.tile0 = chunks->tile_begin[i];
+                kc.num_tiles = chunks->tile_end[i] - chunks->tile_begin[i];
+                if (kc.num_tiles == 0) continue;
+                CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kc, ws, L, s, bucket_in, idx_in, b_lo, rbase)));
+                nl.count += 1;
+            }
+            nl.count -= 1;   // counted once below
+        } else {
+            CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kp, ws, L, s, bucket_in, idx_in, b_lo, rbase)));
+        }
+        tm.mark();
+        k2_coarse_starts<<<1, 1024, 0, s>>>(at<uint32_t>(ws, L.cursor), p.C, at<unsigned long long>(ws, L.starts));
+        CK(cudaGetLastError());
+        tm.mark();
+        // Rank-bucket-level verification (reading A14) is needed only when the network is not
+        // provably monotone: with Eq. 4's sign condition every step of the f32 predictor is a
+        // monotone IEEE operation, so consecutive rank buckets cannot
+        // invert; K5 still checks every coarse-bucket boundary.  Received records (multi-GPU) and
+        // opts->verify == 2 are always verified.
+        const bool verify_fine = GIVEN || verify_all || !monotone(*w);
+        CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, verify_fine, rbase)));
+        tm.mark();
+        k4_big_copy<KeyT, PERM><<<num_sms(), kK3Threads, 0, s>>>(
+            p.capc, p.R, at<KeyT>(ws, L.reg_keys), PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
+            at<unsigned long long>(ws, L.starts), out_keys, out_perm, at<unsigned long long>(ws, L.range_start), dst,
+            at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.flags), &dst->ticket, rbase);
+        CK(cudaGetLastError());
+        tm.mark();
+        k5_boundary_verify<KeyT, PERM><<<(unsigned)((nranges + 255) / 256), 256, 0, s>>>(
+            at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
+        CK(cudaGetLastError());
+        tm.mark();
+        nl.count += (p.local && p.cap1 > 0) ? 6 : 5;
+
+        CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        st = *hs;
+        if (info) {
+            info->num_coarse = p.C;
+            info->tail_lo = st.tail_lo;
+            info->tail_hi = st.tail_hi;
+            info->max_coarse = st.max_coarse;
+            info->big_buckets = st.big_count;
+        }
+        // A region overflowed (the data's coarse-bucket sizes are more skewed than the region
+        // capacity allows): the cursors now hold the exact bucket sizes, so lay the regions out
+        // exactly (16-B aligned starts) and run the pipeline once more.
+        if (st.region_overflow > 0 && attempt == 0 && st.bad_index == ~0ull) {
+            std::vector<uint32_t> sizes(p.C);
+            CK(cudaMemcpy(sizes.data(), at<uint32_t>(ws, L.cursor), (size_t)p.C * 4, cudaMemcpyDeviceToHost));
+            std::vector<unsigned long long> rb(p.C);
+            unsigned long long off = 0;
+            for (uint32_t c = 0; c < p.C; ++c) {
+                rb[c] = off;
+                off += ((unsigned long long)sizes[c] + 7ull) & ~7ull;
+            }
+            if (off <= (unsigned long long)p.C * p.capc) {
+                unsigned long long* d_rb = at<unsigned long long>(ws, L.rbase);
+                CK(cudaMemcpyAsync(d_rb, rb.data(), (size_t)p.C * 8, cudaMemcpyHostToDevice, s));
+                rbase = d_rb;
+                continue;
+            }
+        }
+        break;
     }
+    tm.finish(info);
     if (st.bad_index != ~0ull) {
         if (info) info->bad_index = (int64_t)st.bad_index;
         return MLSORT_ERR_NONFINITE_KEY;
     }
-    uint64_t violations = st.violations;
+    // K5 boundary violations plus violations found inside cluster-K3 slices
+    uint64_t violations = st.violations + st.k3_violations;
     if (st.region_overflow > 0) violations += 1;   // a region was full: use the conventional sort
     if (st.region_overflow == 0 && st.overflow > 0) {   // K4 radix for big buckets that are not all-equal
         std::vector<uint32_t> big(st.big_count), flags(st.big_count);
@@ -855,12 +927,46 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         CK(cudaMemcpyAsync(starts.data(), at<unsigned long long>(ws, L.starts), starts.size() * 8,
                            cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        for (size_t k = 0; k < big.size(); ++k) {
+        // one radix sort over the union of the overflow buckets that still need sorting
+        std::vector<unsigned long long> seg;
+        uint64_t tot = 0;
+        bool all_equal = true;
+        std::vector<uint32_t> order(big.size());
+        for (size_t k = 0; k < big.size(); ++k) order[k] = (uint32_t)k;
+        std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return big[a] < big[b]; });
+        for (uint32_t k : order) {
             const bool equal = flags[k] & 1u;
             if (equal && !PERM) continue;
+            all_equal &= equal;
             const uint64_t S0 = starts[big[k]], len = starts[big[k] + 1] - S0;
-            int rc = radix_segment<KeyT, PERM>(out_keys, out_perm, S0, len, equal, ws, L, s, nl);
-            if (rc) return rc;
+            seg.push_back(S0);
+            seg.push_back(tot);
+            seg.push_back(len);
+            tot += len;
+        }
+        if (tot > 0) {
+            using Bits = typename KeyTraits<KeyT>::Bits;
+            const uint32_t nseg = (uint32_t)(seg.size() / 3);
+            unsigned long long* d_seg = at<unsigned long long>(ws, L.segs);
+            CK(cudaMemcpyAsync(d_seg, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, s));
+            char* rbase = at<char>(ws, L.radix);
+            Bits* k0 = reinterpret_cast<Bits*>(rbase);
+            Bits* k1 = reinterpret_cast<Bits*>(rbase + align_up(tot * sizeof(Bits)));
+            uint32_t* v0 = PERM ? reinterpret_cast<uint32_t*>(rbase + 2 * align_up(tot * sizeof(Bits))) : nullptr;
+            uint32_t* v1 = PERM ? reinterpret_cast<uint32_t*>(rbase + 2 * align_up(tot * sizeof(Bits)) + align_up(tot * 4)) : nullptr;
+            uint32_t* gh = reinterpret_cast<uint32_t*>(rbase + 2 * align_up(tot * sizeof(Bits)) + (PERM ? 2 * align_up(tot * 4) : 0));
+            const int sg = (int)std::min<uint32_t>(nseg, (uint32_t)num_sms() * 8);
+            k_seg_gather<KeyT><<<sg, 256, 0, s>>>(d_seg, nseg, out_keys, out_perm, k0, v0);
+            cudaError_t err;
+            // all-equal perm buckets only need their indices ordered, but buckets hold different
+            // keys, so the key digits are still sorted unless every bucket is all-equal and there
+            // is only one of them
+            const bool skip_keys = all_equal && nseg == 1;
+            int cur = radix_sort_pairs<Bits>(k0, v0, k1, v1, gh, tot, PERM, s, nl, err, skip_keys);
+            if (err != cudaSuccess) return MLSORT_ERR_CUDA;
+            k_seg_scatter<KeyT><<<sg, 256, 0, s>>>(d_seg, nseg, cur ? k1 : k0, cur ? v1 : v0, out_keys, out_perm);
+            CK(cudaGetLastError());
+            nl.count += 2;
         }
         // re-verify every boundary now that all ranges are final
         CK(cudaMemsetAsync(&dst->violations, 0, 8, s));
@@ -868,8 +974,16 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
             at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
         CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        violations = st.violations + hs->violations;
+        // the first K5 pass ran before the overflow buckets were sorted: only the fresh boundary
+        // check counts, together with the slice-internal K3 violations
+        violations = st.k3_violations + hs->violations + (st.region_overflow > 0 ? 1 : 0);
     }
+    if (std::getenv("MLSORT_DEBUG"))
+        fprintf(stderr, "mlsort: plan C=%u fb=%u R=%u local=%d ws=%d group=%d cap=%u cap1=%u | k5=%llu k3=%llu "
+                "region_overflow=%llu overflow=%llu big=%llu local_repairs=%llu -> violations=%llu\n",
+                p.C, p.fb, p.R, (int)p.local, (int)p.ws, (int)p.ws_group, p.cap, p.cap1, st.violations,
+                st.k3_violations, st.region_overflow, st.overflow, st.big_count, st.local_repairs,
+                (unsigned long long)violations);
     if (info) info->repairs = violations + st.local_repairs;
     if (violations > 0) {   // reading A14: escalate to the conventional sort
         if (GIVEN) {
@@ -1026,7 +1140,9 @@ extern "C" int mlsort_sort_host(const void* h_keys, uint64_t n, mlsort_dtype dt,
     const uint64_t B = (o && o->num_buckets) ? o->num_buckets : n;
     ChunkPlan cp;
     if (B <= (1ull << 30) && n < (1ull << 32)) {
-        const Plan pl = make_plan(n, B, ks, h_out_perm != nullptr, true);
+        const Weights* wh = reinterpret_cast<const Weights*>(w);
+        const bool group = wh && want_group(pred_of(o ? o->predictor : 0), mpad_of(wh->m));
+        const Plan pl = make_plan(n, B, ks, h_out_perm != nullptr, true, group);
         const uint32_t nchunk = std::min<uint32_t>(8, pl.T);
         const uint32_t per = (pl.T + nchunk - 1) / nchunk;
         cudaEvent_t start_ev = evs[15];

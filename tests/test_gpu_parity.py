@@ -285,3 +285,17 @@ def test_k8_predictor_monotone_over_all_f32(mls, pred):
         last_y, last_b = float(y[-1]), int(b[-1])
         total += x.numel()
     assert total == 2 * 0x7F800000
+
+
+@pytest.mark.parametrize("n,m", [(1 << 22, 64), (1 << 21, 32)])
+def test_f64_lognormal_large_no_fallback(mls, n, m):
+    """C3-shaped f64 lognormal input at a size whose plan uses the multi-CTA K3 path: exact
+    output, and the path must not need the whole-input conventional-sort fallback."""
+    keys = workloads.generate("lognormal", n, 3, "f64")
+    w, p = _fit(mls, keys, m, n0=1 << 14, seed=3002)
+    import torch
+    k, pm, info = mls.sort(_t(keys), w, perm=False, num_buckets=n // 2)
+    ref_keys, _ = oracle.sorted_reference(keys)
+    np.testing.assert_array_equal(_bits(k.cpu().numpy()), _bits(ref_keys))
+    print("info", info)
+    assert info["fallback_used"] == 0, info
