@@ -302,28 +302,66 @@ def run_multi(args):
     torch.cuda.synchronize()
     dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a2a = []
+    l0 = part.launches + lsort.launches
     with ClockSampler(local) as clk:
         dist.barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
             res = mdist.sort_dist(d_keys, rank * per, n_global, B, part, lsort, with_index=base.perm)
+            a2a.append(res.exchange_ms)
         ev1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
+    launches = part.launches + lsort.launches - l0
     ms = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms], device="cuda")
+    t = torch.tensor([ms, statistics.mean(a2a)], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max, a2a_max = float(t[0].item()), float(t[1].item())
+    # end to end through the same public API from pinned host memory: H2D of the shard, the
+    # distributed sort, D2H of this rank's sorted run (and its global indices)
+    h_keys = torch.from_numpy(keys).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    d2h = 0
+    for _ in range(args.steps):
+        dk = h_keys.to("cuda", non_blocking=True)
+        r = mdist.sort_dist(dk, rank * per, n_global, B, part, lsort, with_index=base.perm)
+        hk = r.keys.to("cpu")
+        d2h = hk.numel() * hk.element_size()
+        if r.index is not None:
+            hi = r.index.to("cpu")
+            d2h += hi.numel() * hi.element_size()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t2 = torch.tensor([e0.elapsed_time(e1) / args.steps, float(d2h)], device="cuda")
+    dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t2[0].item())
+    ks = 4 if base.dtype == "f32" else 8
+    pk = peaks()
+    peak_act = SMS * MUFU_PER_CLK_PER_SM * pk["sm_max_mhz"] * 1e6 / 1e9
+    acts = n_global * base.m
+    achieved = acts / (ms_max * 1e-3) / 1e9 / world          # per GPU
     if rank == 0:
         line = {"metric": METRIC, "value": n_global / (ms_max * 1e-3), "unit": "keys/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": base.dtype, "data": "synthetic",
                 "config": {"workload": f"{base.name}-shaped shard of 2^{int(math.log2(per))} keys per rank, "
                                        f"global N={n_global}, B=N, rank-range all-to-all (NCCL)",
-                           "parallelism": f"dp{world}", "n_global": n_global},
-                "clocks": clk.summary(), "gpu_launches": None,
-                "e2e": None}
+                           "parallelism": f"dp{world}", "n_global": n_global,
+                           "l2": "inputs larger than L2 (126 MB); no flush"},
+                "roofline": {"bound": "alu", "kernel": "whole step per GPU (predict dominates)",
+                             "achieved": achieved, "peak": peak_act, "unit": "Gact/s", "frac": achieved / peak_act,
+                             "traffic": None, "all_to_all_ms": a2a_max,
+                             "peak_source": f"derived: {SMS} SMs x {MUFU_PER_CLK_PER_SM} MUFU/clk x "
+                                            f"{pk['sm_max_mhz']:.0f} MHz"},
+                "e2e": {"value": n_global / (e2e_ms * 1e-3), "unit": "keys/s",
+                        "h2d_bytes_per_step": per * ks * world, "d2h_bytes_per_step": int(t2[1].item()) * world,
+                        "ms_per_step": e2e_ms},
+                "clocks": clk.summary(), "gpu_launches": launches}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 

@@ -71,7 +71,13 @@ def sort_dist(shard, global_offset: int, n_global: int, B: int, partition_fn, lo
     rk, rb, ri, sc = partition_fn(shard, global_offset, n_global, world, B)
     if not with_index:
         ri = None
+    timed = shard.is_cuda
+    if timed:                          # device time of the all-to-all (events on the current stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
     k, b, i, rcounts = exchange(rk, rb, ri, sc, group)
+    if timed:
+        e1.record()
     lo, hi = owner_range(rank, world, B)
     sk, si = local_sort_fn(k, b, i, lo, hi)
     # global offset of this rank's run = number of keys owned by lower ranks
@@ -79,7 +85,11 @@ def sort_dist(shard, global_offset: int, n_global: int, B: int, partition_fn, lo
     allc = [torch.zeros_like(mine) for _ in range(world)]
     dist.all_gather(allc, mine, group=group)
     goff = int(sum(int(c.item()) for c in allc[:rank]))
-    return DistResult(sk, si, goff, sc, rcounts)
+    res = DistResult(sk, si, goff, sc, rcounts)
+    if timed:
+        e1.synchronize()
+        res.exchange_ms = e0.elapsed_time(e1)
+    return res
 
 
 def cuda_partition_fn(weights, predictor: int = 0):
@@ -87,9 +97,11 @@ def cuda_partition_fn(weights, predictor: int = 0):
     import paper_1805_04272_b200 as mls
 
     def fn(shard, goff, n_global, G, B):
-        rk, rb, ri, sc, _info = mls.dist_partition(shard, weights, goff, n_global, G, num_buckets=B,
-                                                    predictor=predictor)
+        rk, rb, ri, sc, info = mls.dist_partition(shard, weights, goff, n_global, G, num_buckets=B,
+                                                   predictor=predictor)
+        fn.launches += int(info.get("kernel_launches", 0))
         return rk, rb, ri, sc
+    fn.launches = 0                    # kernel launches issued so far (bench accounting)
     return fn
 
 
@@ -97,6 +109,8 @@ def cuda_local_sort_fn():
     import paper_1805_04272_b200 as mls
 
     def fn(k, b, i, lo, hi):
-        sk, si, _info = mls.sort_records(k, b, i, lo, hi)
+        sk, si, info = mls.sort_records(k, b, i, lo, hi)
+        fn.launches += int(info.get("kernel_launches", 0))
         return sk, si
+    fn.launches = 0
     return fn
