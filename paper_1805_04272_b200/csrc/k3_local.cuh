@@ -47,7 +47,7 @@ __device__ unsigned long long g_k3l_phase[1024][8];
 
 constexpr int kL3Threads = 512;         // primary pass: two CTAs per SM
 constexpr int kL3ThreadsBig = 1024;     // secondary pass (larger coarse buckets): one CTA per SM
-constexpr uint32_t kL3RankMax = 64;     // rank buckets up to this size: rank by counting
+constexpr uint32_t kL3RankMax = 24;     // rank buckets up to this size: insertion sort by one thread
 constexpr uint32_t kL3BigQ = 48;        // queued larger rank buckets per coarse bucket
 
 struct K3LParams {
@@ -65,19 +65,22 @@ struct K3LParams {
 // exceeds 65535 elements here); words rounded up to 4 so the key array after it is 16-B aligned.
 __host__ __device__ inline uint32_t k3l_hist_words(uint32_t kfine) { return ((kfine + 1u) / 2u + 3u) & ~3u; }
 
-// smem: ctrl | hist (u16 pairs) | skey[cap] | sidx[cap] (perm) | sfine[cap] u16
-inline size_t k3l_smem_bytes(size_t ks, bool perm, uint32_t kfine, uint32_t cap) {
-    return kCtrlBytes + (size_t)k3l_hist_words(kfine) * 4 + (size_t)cap * ks + (perm ? (size_t)cap * 4 : 0) +
-           (size_t)cap * 2;
+constexpr uint32_t kL3WarpQ = 64;       // per-warp fix-up queue entries (power of two)
+__host__ __device__ constexpr size_t k3l_queue_bytes(int nt) { return (size_t)(nt / 32) * kL3WarpQ * 4; }
+
+// smem: ctrl | per-warp fix-up queues | hist (u16 pairs) | skey[cap] | sidx[cap] (perm)
+inline size_t k3l_smem_bytes(size_t ks, bool perm, uint32_t kfine, uint32_t cap, int nt) {
+    return kCtrlBytes + k3l_queue_bytes(nt) + (size_t)k3l_hist_words(kfine) * 4 + (size_t)cap * ks +
+           (perm ? (size_t)cap * 4 : 0);
 }
 
 // largest cap with k3l_smem_bytes(...) <= budget
-inline uint32_t k3l_cap_for(size_t budget, size_t ks, bool perm, uint32_t kfine) {
-    const size_t fixed = kCtrlBytes + (size_t)k3l_hist_words(kfine) * 4;
+inline uint32_t k3l_cap_for(size_t budget, size_t ks, bool perm, uint32_t kfine, int nt) {
+    const size_t fixed = kCtrlBytes + k3l_queue_bytes(nt) + (size_t)k3l_hist_words(kfine) * 4;
     if (budget <= fixed) return 0;
-    const size_t leb = ks + (perm ? 4 : 0) + 2;
+    const size_t leb = ks + (perm ? 4 : 0);
     uint64_t cap = std::min<uint64_t>((budget - fixed) / leb, 65535ull);
-    while (cap > 0 && k3l_smem_bytes(ks, perm, kfine, (uint32_t)cap) > budget) --cap;
+    while (cap > 0 && k3l_smem_bytes(ks, perm, kfine, (uint32_t)cap, nt) > budget) --cap;
     return (uint32_t)cap;
 }
 
@@ -141,6 +144,137 @@ template <> __device__ __forceinline__ void load8<double>(const double* p, doubl
 }
 
 
+// compare-exchange of (key, index) records in registers: afterwards (ka, ia) precedes (kb, ib)
+template <typename KeyT, bool PERM>
+__device__ __forceinline__ void k3l_cx(typename KeyTraits<KeyT>::Bits& ka, uint32_t& ia,
+                                       typename KeyTraits<KeyT>::Bits& kb, uint32_t& ib) {
+    using Bits = typename KeyTraits<KeyT>::Bits;
+    if (!PERM) {
+        const Bits lo = ka < kb ? ka : kb, hi = ka < kb ? kb : ka;
+        ka = lo;
+        kb = hi;
+    } else {
+        const bool sw = kb < ka || (kb == ka && ib < ia);
+        const Bits tk = sw ? kb : ka;
+        kb = sw ? ka : kb;
+        ka = tk;
+        const uint32_t ti = sw ? ib : ia;
+        ib = sw ? ia : ib;
+        ia = ti;
+    }
+}
+
+// sort the 2..N records at [s, s + len) in place (N = 4 or 8): pad to N with the maximum
+// record (it sorts last, so the first len outputs are the bucket), then Batcher's odd-even
+// merge network (5 / 19 comparators) in registers
+template <typename KeyT, bool PERM, int N>
+__device__ __forceinline__ void k3l_sortn(typename KeyTraits<KeyT>::Bits* key, uint32_t* idx, uint32_t s,
+                                          uint32_t len) {
+    using Bits = typename KeyTraits<KeyT>::Bits;
+    Bits k[N];
+    uint32_t i[N];
+#pragma unroll
+    for (uint32_t q = 0; q < N; ++q) {
+        k[q] = q < len ? key[s + q] : ~(Bits)0;
+        i[q] = PERM ? (q < len ? idx[s + q] : 0xffffffffu) : 0u;
+    }
+#define K3L_CX(a, b) k3l_cx<KeyT, PERM>(k[a], i[a], k[b], i[b])
+    if (N == 4) {
+        K3L_CX(0, 1); K3L_CX(2, 3);
+        K3L_CX(0, 2); K3L_CX(1, 3);
+        K3L_CX(1, 2);
+    } else {
+        K3L_CX(0, 1); K3L_CX(2, 3); K3L_CX(4, 5); K3L_CX(6, 7);
+        K3L_CX(0, 2); K3L_CX(1, 3); K3L_CX(4, 6); K3L_CX(5, 7);
+        K3L_CX(1, 2); K3L_CX(5, 6);
+        K3L_CX(0, 4); K3L_CX(1, 5); K3L_CX(2, 6); K3L_CX(3, 7);
+        K3L_CX(2, 4); K3L_CX(3, 5);
+        K3L_CX(1, 2); K3L_CX(3, 4); K3L_CX(5, 6);
+    }
+#undef K3L_CX
+#pragma unroll
+    for (uint32_t q = 0; q < N; ++q) {
+        if (q < len) {
+            key[s + q] = k[q];
+            if (PERM) idx[s + q] = i[q];
+        }
+    }
+}
+
+// stable insertion sort of [s, e) in shared memory by one thread (short runs: the cost is the
+// run length plus its inversions; `top`, the largest record so far, stays in registers)
+template <typename KeyT, bool PERM>
+__device__ __forceinline__ void k3l_insertion(typename KeyTraits<KeyT>::Bits* key, uint32_t* idx, uint32_t s,
+                                              uint32_t e) {
+    using Bits = typename KeyTraits<KeyT>::Bits;
+    if (e <= s + 1) return;
+    Bits top = key[s];
+    uint32_t topi = PERM ? idx[s] : 0u;
+    for (uint32_t i = s + 1; i < e; ++i) {
+        const Bits k = key[i];
+        const uint32_t x = PERM ? idx[i] : 0u;
+        if (precedes<KeyT, PERM>(k, x, top, topi)) {
+            uint32_t j = i;
+            key[j] = top;
+            if (PERM) idx[j] = topi;
+            --j;
+            while (j > s && precedes<KeyT, PERM>(k, x, key[j - 1], PERM ? idx[j - 1] : 0u)) {
+                key[j] = key[j - 1];
+                if (PERM) idx[j] = idx[j - 1];
+                --j;
+            }
+            key[j] = k;
+            if (PERM) idx[j] = x;
+        } else {
+            top = k;
+            topi = x;
+        }
+    }
+}
+
+template <typename T> struct K3Out { using Bits = T; __device__ static T conv(T v) { return v; } };
+template <> struct K3Out<float> {
+    using Bits = uint32_t;
+    __device__ static float conv(uint32_t v) { return KeyTraits<float>::from_ord(v); }
+};
+template <> struct K3Out<double> {
+    using Bits = unsigned long long;
+    __device__ static double conv(unsigned long long v) { return KeyTraits<double>::from_ord(v); }
+};
+
+// out[0, n) = conv(src[0, n)) with 16-byte stores (scalar head up to the first aligned slot)
+template <typename T, int NT>
+__device__ __forceinline__ void k3l_store(const typename K3Out<T>::Bits* src, uint32_t n, T* out) {
+    constexpr uint32_t V = 16 / sizeof(T);
+    const uint32_t head = min(n, (uint32_t)(((16u - ((uint32_t)reinterpret_cast<uintptr_t>(out) & 15u)) & 15u) / sizeof(T)));
+    if (threadIdx.x < head) out[threadIdx.x] = K3Out<T>::conv(src[threadIdx.x]);
+    const uint32_t nv = (n - head) / V;
+    T* o = out + head;
+    const typename K3Out<T>::Bits* sp = src + head;
+    for (uint32_t v = threadIdx.x; v < nv; v += NT) {
+        if (V == 4) {
+            float4 q;
+            uint32_t* qq = reinterpret_cast<uint32_t*>(&q);
+#pragma unroll
+            for (uint32_t c = 0; c < 4; ++c) {
+                const T t = K3Out<T>::conv(sp[4 * v + c]);
+                qq[c] = *reinterpret_cast<const uint32_t*>(&t);
+            }
+            reinterpret_cast<float4*>(o)[v] = q;
+        } else {
+            double2 q;
+            unsigned long long* qq = reinterpret_cast<unsigned long long*>(&q);
+#pragma unroll
+            for (uint32_t c = 0; c < 2; ++c) {
+                const T t = K3Out<T>::conv(sp[2 * v + c]);
+                qq[c] = *reinterpret_cast<const unsigned long long*>(&t);
+            }
+            reinterpret_cast<double2*>(o)[v] = q;
+        }
+    }
+    for (uint32_t i = head + nv * V + threadIdx.x; i < n; i += NT) out[i] = K3Out<T>::conv(src[i]);
+}
+
 template <typename KeyT, bool PERM, int NT>
 __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
 k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __restrict__ reg_fine,
@@ -151,21 +285,22 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
               unsigned long long* __restrict__ ticket, const unsigned long long* __restrict__ rbase) {
     using Bits = typename KeyTraits<KeyT>::Bits;
     extern __shared__ __align__(16) unsigned char smem[];
-    // ctrl words: [1] next ticket, [2] big-queue count, [8..40) scan scratch,
-    // [64 .. 64+3*kL3BigQ) big-queue (start, end, rank bucket) triples
+    // ctrl words: [1] next ticket, [2] big-queue count, [8..72) scan scratch,
+    // [80 .. 80+2*kL3BigQ) big-queue (start, end) pairs
     uint32_t* ctrl = reinterpret_cast<uint32_t*>(smem);
     uint32_t* scratch = ctrl + 8;
-    uint32_t* bigq = ctrl + 64;
-    uint32_t* h2 = reinterpret_cast<uint32_t*>(smem + kCtrlBytes);          // u16 counter pairs
+    uint32_t* bigq = ctrl + 80;
+    uint32_t* wqueue = reinterpret_cast<uint32_t*>(smem + kCtrlBytes);
+    uint32_t* h2 = reinterpret_cast<uint32_t*>(smem + kCtrlBytes + k3l_queue_bytes(NT));   // u16 counter pairs
     Bits* skey = reinterpret_cast<Bits*>(h2 + k3l_hist_words(p.kfine));
     uint32_t* sidx = reinterpret_cast<uint32_t*>(skey + p.cap);
-    uint16_t* sfine = reinterpret_cast<uint16_t*>(sidx + (PERM ? p.cap : 0));
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // work items: coarse ids 0..C-1 (primary) or mid_list[0..mid_count) (secondary)
     const uint32_t items = p.secondary ? (uint32_t)st->mid_count : p.num_coarse;
     auto coarse_of = [&](uint32_t t) { return p.secondary ? mid_list[t] : t; };
     const uint32_t hw = (p.kfine + 1u) / 2u;           // histogram words
+    const uint32_t hwp = k3l_hist_words(p.kfine);      // padded to a multiple of 4
     if (tid == 0) {
         const uint32_t t0 = (uint32_t)atomicAdd(ticket, 1ull);
         ctrl[1] = t0;
@@ -227,7 +362,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         const uint4* g8 = reinterpret_cast<const uint4*>(gf);
 
         // ---- 1. histogram of rank buckets (8 ids per 128-bit load; rows are 16-B aligned)
-        for (uint32_t w = tid; w < hw; w += NT) h2[w] = 0u;
+        for (uint32_t w = tid; w < hwp; w += NT) h2[w] = 0u;
         __syncthreads();
         {
             uint32_t i = tid;
@@ -241,55 +376,53 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         }
         __syncthreads();
         K3L_T(1);
-        // ---- 2. exclusive scan of the counters: warp w owns a contiguous chunk of words; 8 rows
-        // of 32 words are loaded and warp-scanned independently (ILP), then chained by their
-        // totals; finally the warp totals are scanned across the CTA
+        // ---- 2. exclusive scan of the counters: thread t scans its own WPT consecutive words
+        // (128-bit loads, WPT a multiple of 4) in registers, then one block-wide scan of the
+        // per-thread totals
         {
-            constexpr int kW = NT / 32;
-            const uint32_t chunk = (((hw + kW - 1) / kW) + 31u) & ~31u;
-            const uint32_t b0 = min(hw, (uint32_t)warp * chunk), b1 = min(hw, b0 + chunk);
-            uint32_t carry = 0;
-            for (uint32_t r0 = b0; r0 < b1; r0 += 256) {
-                uint32_t v[8], x[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t w = r0 + 32 * k + lane;
-                    v[k] = w < b1 ? h2[w] : 0u;
-                    x[k] = (v[k] & 0xffffu) + (v[k] >> 16);
-                }
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const uint32_t yy = __shfl_up_sync(0xffffffffu, x[k], o);
-                        if (lane >= o) x[k] += yy;
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t w = r0 + 32 * k + lane;
-                    const uint32_t lo = v[k] & 0xffffu;
-                    const uint32_t ex = carry + x[k] - (lo + (v[k] >> 16));
-                    if (w < b1) h2[w] = ex | ((ex + lo) << 16);
-                    carry += __shfl_sync(0xffffffffu, x[k], 31);
-                }
+            const uint32_t wpt = (((hwp + NT - 1) / NT) + 3u) & ~3u;
+            const uint32_t tw0 = min(hwp, (uint32_t)tid * wpt), tw1 = min(hwp, tw0 + wpt);
+            uint4* h8 = reinterpret_cast<uint4*>(h2);
+            uint32_t tot = 0;
+            for (uint32_t w = tw0; w < tw1; w += 4) {
+                const uint4 v = h8[w >> 2];
+                tot += (v.x & 0xffffu) + (v.x >> 16) + (v.y & 0xffffu) + (v.y >> 16) + (v.z & 0xffffu) +
+                       (v.z >> 16) + (v.w & 0xffffu) + (v.w >> 16);
             }
-            if (lane == 0) scratch[warp] = carry;
+            uint32_t x = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t yy = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += yy;
+            }
+            if (lane == 31) scratch[warp] = x;
             __syncthreads();
             if (warp == 0) {
+                constexpr int kW = NT / 32;
                 const uint32_t tt = lane < kW ? scratch[lane] : 0u;
-                uint32_t x = tt;
+                uint32_t z = tt;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t yy = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += yy;
+                    const uint32_t yy = __shfl_up_sync(0xffffffffu, z, o);
+                    if (lane >= o) z += yy;
                 }
-                if (lane < kW) scratch[lane] = x - tt;
+                if (lane < kW) scratch[32 + lane] = z - tt;
             }
             __syncthreads();
-            const uint32_t add = scratch[warp];
-            if (add)
-                for (uint32_t w = b0 + lane; w < b1; w += 32) h2[w] += add | (add << 16);
+            uint32_t run = scratch[32 + warp] + x - tot;
+            auto ex2 = [&](uint32_t v) {               // two counters -> two exclusive starts
+                const uint32_t lo = v & 0xffffu, r = run | ((run + lo) << 16);
+                run += lo + (v >> 16);
+                return r;
+            };
+            for (uint32_t w = tw0; w < tw1; w += 4) {
+                uint4 v = h8[w >> 2];
+                v.x = ex2(v.x);
+                v.y = ex2(v.y);
+                v.z = ex2(v.z);
+                v.w = ex2(v.w);
+                h8[w >> 2] = v;
+            }
         }
         __syncthreads();
         K3L_T(2);
@@ -311,7 +444,6 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
                 const uint32_t f = (fw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
                 const uint32_t pos = hist_inc_ret(h2, f);
                 skey[pos] = KeyTraits<KeyT>::to_ord(kv[k]);
-                sfine[pos] = (uint16_t)f;
                 if (PERM) sidx[pos] = iv[k];
             }
         }
@@ -319,116 +451,87 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             const uint32_t f = gf[q];
             const uint32_t pos = hist_inc_ret(h2, f);
             skey[pos] = KeyTraits<KeyT>::to_ord(gk[q]);
-            sfine[pos] = (uint16_t)f;
             if (PERM) sidx[pos] = gi[q];
         }
         __syncthreads();                       // counter f = end of rank bucket f
         K3L_T(3);
-        // ---- 4. fix-up fused with the store ("only the numbers inside each bucket need to
-        // be sorted"): each position ranks its element inside its rank bucket [s, e) by counting
-        // the elements that precede it under (totalOrder key, index) and writes it to its final
-        // output position.  Buckets of <= 4 elements (98 % of the keys for a Poisson(1) fill) use
-        // a fixed predicated compare sequence, up to kL3RankMax a loop, larger ones are queued
-        // for a block-wide sort.
-        for (uint32_t pos = tid; pos < n; pos += NT) {
-            const uint32_t f = sfine[pos];
-            const uint32_t e = hist_get(h2, f), s = f ? hist_get(h2, f - 1) : 0u;
-            const uint32_t len = e - s;
-            const Bits kv = skey[pos];
-            const uint32_t iv = PERM ? sidx[pos] : pos;
-            uint32_t rank = 0;
-#if defined(MLSORT_K3L_EXPT) && MLSORT_K3L_EXPT == 2
-            if (false) {                       // experiment: no ranking
-#else
-            if (len > 1) {
-#endif
-                if (len <= 4) {                // the common case: fixed, predicated compares
+        // ---- 4. fix-up in place ("only the numbers inside each bucket need to be sorted").
+        // Warp v walks 32 counter words (64 rank buckets) per batch.  Buckets of 0-1 elements
+        // (~70 % of them) need nothing; those of 2-4 are compacted into a per-warp queue (ballot +
+        // prefix) and sorted 32 at a time, one per lane, by a padded 4-element network in
+        // registers; 5..8 elements (rare) by an 8-element network and up to kL3RankMax by insertion
+        // in their own lane, longer ones
+        // (tails clamped into the end buckets, heavy duplicates) queued for a block-wide sort.
+        {
+            uint32_t* wq = wqueue + warp * kL3WarpQ;
+            uint32_t qn = 0, qd = 0;                   // warp-uniform: entries queued / sorted
+            const uint32_t lt = (1u << lane) - 1u;
+            for (uint32_t wb = (uint32_t)warp * 32u; wb < hw; wb += NT) {
+                const uint32_t w = wb + lane;
+                uint32_t sb[2] = {0u, 0u}, len[2] = {0u, 0u};
+                if (w < hw) {
+                    const uint32_t v = h2[w];
+                    sb[0] = w ? (h2[w - 1] >> 16) : 0u;
+                    sb[1] = v & 0xffffu;
+                    len[0] = sb[1] - sb[0];
+                    len[1] = (v >> 16) - sb[1];
+                }
 #pragma unroll
-                    for (uint32_t q = 0; q < 4; ++q) {
-                        if (q < len) {
-                            const Bits kq = skey[s + q];
-                            const uint32_t iq = PERM ? sidx[s + q] : s + q;
-                            rank += (kq < kv || (kq == kv && iq < iv)) ? 1u : 0u;
+                for (int h = 0; h < 2; ++h) {
+                    if (len[h] > 4u) {                 // rare: sorted by their own lane
+                        if (len[h] <= 8u) {
+                            k3l_sortn<KeyT, PERM, 8>(skey, sidx, sb[h], len[h]);
+                        } else if (len[h] <= kL3RankMax) {
+                            k3l_insertion<KeyT, PERM>(skey, sidx, sb[h], sb[h] + len[h]);
+                        } else {
+                            const uint32_t q = atomicAdd(&ctrl[2], 1u);
+                            if (q < kL3BigQ) {
+                                bigq[2 * q] = sb[h];
+                                bigq[2 * q + 1] = sb[h] + len[h];
+                            }
                         }
                     }
-                } else if (len <= kL3RankMax) {
-                    for (uint32_t q = s; q < e; ++q) {
-                        const Bits kq = skey[q];
-                        const uint32_t iq = PERM ? sidx[q] : q;
-                        rank += (kq < kv || (kq == kv && iq < iv)) ? 1u : 0u;
+                    const bool need = len[h] - 2u <= 2u;
+                    const uint32_t m = __ballot_sync(0xffffffffu, need);
+                    if (need) wq[(qn + __popc(m & lt)) & (kL3WarpQ - 1u)] = sb[h] | (len[h] << 16);
+                    qn += __popc(m);
+                    __syncwarp();
+                    if (qn - qd >= 32u) {
+                        const uint32_t ent = wq[(qd + lane) & (kL3WarpQ - 1u)];
+                        k3l_sortn<KeyT, PERM, 4>(skey, sidx, ent & 0xffffu, ent >> 16);
+                        qd += 32u;
+                        __syncwarp();
                     }
-                } else {                       // large bucket: block-wide sort below
-                    if (pos == s) {
-                        const uint32_t q = atomicAdd(&ctrl[2], 1u);
-                        if (q < kL3BigQ) {
-                            bigq[3 * q] = s;
-                            bigq[3 * q + 1] = e;
-                            bigq[3 * q + 2] = f;
-                        }
-                    }
-                    continue;
                 }
             }
-#if defined(MLSORT_K3L_EXPT) && MLSORT_K3L_EXPT == 1
-            if (rank == 0xffffffffu) out_keys[S0] = KeyTraits<KeyT>::from_ord(kv);   // experiment: no store
-#else
-            out_keys[S0 + s + rank] = KeyTraits<KeyT>::from_ord(kv);
-            if (PERM) out_perm[S0 + s + rank] = iv;
-#endif
+            if (lane < qn - qd) {
+                const uint32_t ent = wq[(qd + lane) & (kL3WarpQ - 1u)];
+                k3l_sortn<KeyT, PERM, 4>(skey, sidx, ent & 0xffffu, ent >> 16);
+            }
         }
         __syncthreads();
         K3L_T(4);
         // ---- 5. large rank buckets (tails collected in the end buckets, heavy duplicates):
-        // block-wide bitonic sort in shared memory, then store
+        // block-wide bitonic sort in shared memory
         const uint32_t nbig = ctrl[2];
-        if (nbig <= kL3BigQ) {
-            for (uint32_t q = 0; q < nbig; ++q) {
-                const uint32_t s = bigq[3 * q], e = bigq[3 * q + 1];
-                block_bitonic_sort_nt<KeyT, PERM, NT>(skey, sidx, s, e);
-                for (uint32_t i = s + tid; i < e; i += NT) {
-                    out_keys[S0 + i] = KeyTraits<KeyT>::from_ord(skey[i]);
-                    if (PERM) out_perm[S0 + i] = sidx[i];
-                }
-            }
-        }
-        __syncthreads();                       // this CTA's output stores are visible to it
+        if (nbig <= kL3BigQ)
+            for (uint32_t q = 0; q < nbig; ++q) block_bitonic_sort_nt<KeyT, PERM, NT>(skey, sidx, bigq[2 * q], bigq[2 * q + 1]);
         K3L_T(5);
-        // ---- 5b. weights not provably monotone: verify every rank-bucket boundary on the stored
-        // output (the last element of every non-empty bucket against the first of the next one)
+        // ---- 5b. weights not provably monotone: check the whole coarse bucket in shared memory
+        // (every rank bucket is sorted, so only rank-bucket boundaries can be out of order)
         bool bad = false;
-        for (uint32_t f0 = tid; p.verify && f0 < p.kfine; f0 += 4 * NT) {
-            Bits ka[4], kb[4];
-            uint32_t ia[4], ib[4];
-            bool chk[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t f = f0 + u * NT;
-                const uint32_t e = f < p.kfine ? hist_get(h2, f) : 0u;
-                const uint32_t s = (f < p.kfine && f) ? hist_get(h2, f - 1) : 0u;
-                chk[u] = e > s && e < n;
-                if (chk[u]) {
-                    ka[u] = KeyTraits<KeyT>::to_ord(out_keys[S0 + e - 1]);
-                    kb[u] = KeyTraits<KeyT>::to_ord(out_keys[S0 + e]);
-                    if (PERM) {
-                        ia[u] = out_perm[S0 + e - 1];
-                        ib[u] = out_perm[S0 + e];
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (chk[u]) bad |= PERM ? !precedes<KeyT, true>(ka[u], ia[u], kb[u], ib[u]) : (kb[u] < ka[u]);
-        }
+        if (p.verify)
+            for (uint32_t i = tid + 1; i < n; i += NT)
+                bad |= precedes<KeyT, PERM>(skey[i], PERM ? sidx[i] : 0u, skey[i - 1], PERM ? sidx[i - 1] : 0u);
         // ---- 6. an inversion between rank buckets (ulp-level non-monotone network output, or a
         // non-monotone model), or too many large buckets: sort the whole coarse bucket
         if (__syncthreads_or(bad) || nbig > kL3BigQ) {
             block_bitonic_sort_nt<KeyT, PERM, NT>(skey, sidx, 0, n);
-            for (uint32_t i = tid; i < n; i += NT) {
-                out_keys[S0 + i] = KeyTraits<KeyT>::from_ord(skey[i]);
-                if (PERM) out_perm[S0 + i] = sidx[i];
-            }
             if (tid == 0 && nbig <= kL3BigQ) atomicAdd(&st->local_repairs, 1ull);
         }
+        // ---- 7. coalesced store of the sorted coarse bucket to its output range
+        k3l_store<KeyT, NT>(skey, n, out_keys + S0);
+        if (PERM) k3l_store<uint32_t, NT>(sidx, n, out_perm + S0);
         K3L_T(6);
     }
 #ifdef MLSORT_K3L_TIMING

@@ -332,7 +332,7 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
         const bool ws_fits = allow_ws && k1ws_smem_bytes(ks, ws_tile_of(ks), (uint32_t)C) <= kK1WsSmemMax;
         if (k1 > kK1SmemMax && !ws_fits) continue;
         const uint32_t kfine = 1u << fb;
-        const uint64_t cap = k3l_cap_for(kK3LSmemMax, ks, perm, kfine);
+        const uint64_t cap = k3l_cap_for(kK3LSmemMax, ks, perm, kfine, kL3ThreadsBig);
         const double avg = (double)n * (double)kfine / (double)B;
         if ((double)cap < 2.0 * avg + 64.0) continue;
         p.local = true;
@@ -343,11 +343,11 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
         p.kfine = kfine;
         p.cap = (uint32_t)cap;
         p.k1_smem = k1;
-        p.k3_smem = k3l_smem_bytes(ks, perm, kfine, (uint32_t)cap);
+        p.k3_smem = k3l_smem_bytes(ks, perm, kfine, (uint32_t)cap, kL3ThreadsBig);
         // two-CTA primary pass only when it holds the average bucket with margin
-        p.cap1 = k3l_cap_for(kK3LSmemPrimary, ks, perm, kfine);
-        if ((double)p.cap1 < 1.25 * avg + 64.0) p.cap1 = 0;
-        p.k3_smem1 = p.cap1 ? k3l_smem_bytes(ks, perm, kfine, p.cap1) : 0;
+        p.cap1 = k3l_cap_for(kK3LSmemPrimary, ks, perm, kfine, kL3Threads);
+        if ((double)p.cap1 < 1.15 * avg + 64.0) p.cap1 = 0;
+        p.k3_smem1 = p.cap1 ? k3l_smem_bytes(ks, perm, kfine, p.cap1, kL3Threads) : 0;
         uint64_t cc = (uint64_t)std::ceil(kRegionFactor * avg) + 64;
         cc = (cc + 7) & ~7ull;
         p.capc = (uint32_t)std::min<uint64_t>(cc, 0xFFFFFFF0ull);

@@ -66,11 +66,11 @@ int main() {
     kp.num_coarse = C;
     kp.kfine = kfine;
     const int NTB = getenv("K3_NT512") ? 512 : 1024;
-    kp.cap = k3l_cap_for(NTB == 512 ? 115712 : 232448, 4, false, kfine);
+    kp.cap = k3l_cap_for(NTB == 512 ? 115712 : 232448, 4, false, kfine, NTB);
     kp.verify = getenv("K3_VERIFY") ? 1 : 0;
     kp.secondary = 0;
     kp.to_mid = 0;
-    const size_t sm = k3l_smem_bytes(4, false, kfine, kp.cap);
+    const size_t sm = k3l_smem_bytes(4, false, kfine, kp.cap, NTB);
     auto kern = NTB == 512 ? k3_local_sort<float, false, 512> : k3_local_sort<float, false, 1024>;
     const int grid = NTB == 512 ? 296 : 148;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -83,7 +83,7 @@ int main() {
         cudaMemset(big_mark, 0, C * 4);
         cudaEventRecord(a);
         kern<<<grid, NTB, sm>>>(kp, rk, rf, nullptr, d_starts, out, nullptr, range_start, st, big_list, big_mark,
-                                      mid_list, &st->ticket3);
+                                      mid_list, &st->ticket3, nullptr);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
@@ -95,8 +95,8 @@ int main() {
     // per-phase cycles (last run), averaged over CTAs, per coarse bucket
     static unsigned long long ph[1024][8];
     cudaMemcpyFromSymbol(ph, g_k3l_phase, sizeof(ph));
-    const char* names[8] = {"loop top / ticket", "zero+hist", "scan", "placement", "fixup+store", "big buckets",
-                            "verify+repair", "-"};
+    const char* names[8] = {"loop top / ticket", "zero+hist", "scan", "placement", "fixup in smem", "big buckets",
+                            "verify+store", "-"};
     double tot = 0;
     for (int i = 0; i < 7; ++i) {
         double sum = 0;
