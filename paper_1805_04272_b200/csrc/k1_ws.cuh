@@ -65,9 +65,10 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.a
 // class order.
 template <typename KeyT, int MPAD, int PRED, bool PERM, int KGW = 8, bool PARTITION = true, bool GROUP = false>
 __global__ void __launch_bounds__(WsCfg<KeyT, GROUP>::kThreads, 1)
-k1_ws(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p, KeyT* __restrict__ reg_keys,
+k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
       uint16_t* __restrict__ reg_fine, uint32_t* __restrict__ reg_idx, uint32_t* __restrict__ cursor,
-      DevStatus* __restrict__ st, const unsigned long long* __restrict__ rbase) {
+      DevStatus* __restrict__ st, const unsigned long long* __restrict__ rbase, FoldedWeights fw) {
+    // (fw last: its hot members then sit in the first 4 KB of the parameter bank)
     using Cfg = WsCfg<KeyT, GROUP>;
     constexpr int T = Cfg::kT;
     constexpr int KPT = Cfg::kKPT;

@@ -122,11 +122,15 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
             f.C[j] = (float)(w.beta[o] * (w.w1[o] + w.b[o]) * log2e + A * (x0 - w.lo));
             f.W[j] = (float)(w.w2[o] * scale);
             f.Wn[j] = -f.W[j];
+            f.Cs[j] = (float)((double)f.C[j] - (double)kAShift);
+            f.Wns[j] = std::ldexp(f.Wn[j], -(int)kAShift);
         } else {
             f.A[j] = 0.0f;
             f.C[j] = 0.0f;
             f.W[j] = 0.0f;   // pad neurons contribute nothing
             f.Wn[j] = 0.0f;
+            f.Cs[j] = -kAShift;
+            f.Wns[j] = 0.0f;
         }
     }
     // ---- saturated-pair skipping bounds and constants (predict.cuh gvm_forward_skip)
@@ -198,14 +202,16 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
         }
         f.lut[i] = (unsigned char)cls;
     }
-    // safe range of u for the clamp-free predictor: a_j = A_j u + C_j <= 59 for every neuron
-    // (the f32 FFMA's rounding is far below the 59 -> 125 margin of the reciprocal chain)
+    // safe range of u for the clamp-free packed predictor: A_j u + Cs_j <= kAClamp - 1 for every
+    // neuron (the f32 FFMA's rounding is far below the margin of the reciprocal chain, whose d
+    // stays normal up to a - s = 125)
     double ulo = -INFINITY, uhi = INFINITY;
+    const double amax = (double)kAClamp - 1.0;
     for (uint32_t j = 0; j < mpad; ++j) {
-        const double A = f.A[j], C = f.C[j];
-        if (A < 0) ulo = std::max(ulo, (59.0 - C) / A);
-        else if (A > 0) uhi = std::min(uhi, (59.0 - C) / A);
-        else if (C > 59.0) { ulo = INFINITY; uhi = -INFINITY; }
+        const double A = f.A[j], C = f.Cs[j];
+        if (A < 0) ulo = std::max(ulo, (amax - C) / A);
+        else if (A > 0) uhi = std::min(uhi, (amax - C) / A);
+        else if (C > amax) { ulo = INFINITY; uhi = -INFINITY; }
     }
     f.u_safe_lo = ulo == -INFINITY ? -INFINITY : (float)std::nextafter((float)ulo, INFINITY);
     f.u_safe_hi = uhi == INFINITY ? INFINITY : (float)std::nextafter((float)uhi, -INFINITY);
@@ -218,7 +224,7 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
     f.one2 = pair(1.0f);
     f.k1_2 = pair(2.001281198f);
     f.magic2 = pair(12582912.0f);
-    f.pad2 = 0;
+    f.dofs2 = pair(std::ldexp(1.0f, -(int)kAShift));
     return f;
 }
 
@@ -513,9 +519,9 @@ cudaError_t launch_k1_ws_t(const Plan& p, const KeyT* keys, const FoldedWeights&
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k1_smem);
     if (e != cudaSuccess) return e;
     const int grid = std::min<int>(num_sms(), (int)kp.num_tiles);
-    kern<<<grid, ws_threads(group), p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
+    kern<<<grid, ws_threads(group), p.k1_smem, s>>>(keys, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
                                              PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr, at<uint32_t>(ws, L.cursor),
-                                             at<DevStatus>(ws, L.status), rbase);
+                                             at<DevStatus>(ws, L.status), rbase, fw);
     return cudaGetLastError();
 }
 

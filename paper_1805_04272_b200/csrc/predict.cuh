@@ -22,12 +22,17 @@ constexpr int kMaxM = 64;
 // Passed by value: lives in the kernel-parameter constant bank, so every FFMA reads its
 // weight operand straight from constant memory (warp-uniform, no LDS).
 struct __align__(16) FoldedWeights {
+    // (c, c) pairs of the packed predictor's constants, read from the parameter bank (uniform
+    // registers) instead of occupying vector register pairs: 1, k1, 1.5*2^23, 2^-kAShift.
+    // The hot members come first: the whole struct is a kernel parameter and only the first
+    // 4 KB of the parameter bank are addressed directly by the instructions that read them.
+    unsigned long long one2, k1_2, magic2, dofs2;
     float A[kMaxM];
-    float C[kMaxM];
-    float W[kMaxM];    // w2_j * 2^S (fixed-point accumulation scale, see below)
-    float Wn[kMaxM];   // -W_j (the packed predictor carries -1/d)
-    // u in [u_safe_lo, u_safe_hi] keeps every argument a_j = A_j u + C_j <= 59, so the packed
-    // predictor may skip its per-activation clamp for such keys (CLAMP = false)
+    // packed predictor, exponent-shifted (see kAShift): Cs_j = C_j - kAShift, Wns_j = -W_j 2^-kAShift
+    float Cs[kMaxM];
+    float Wns[kMaxM];
+    // u in [u_safe_lo, u_safe_hi] keeps every shifted argument A_j u + Cs_j <= kAClamp, so the
+    // packed predictor may skip its per-activation clamp for such keys (CLAMP = false)
     float u_safe_lo, u_safe_hi, pad_f[2];
     // Saturated-pair skipping.  Neurons are stored sorted by
     // centre.  For u < lo2[p] both neurons of pair p have a > 24.5 or a < -26.5 on their left
@@ -36,11 +41,11 @@ struct __align__(16) FoldedWeights {
     // reciprocal chain returns its value at d = 1), whose float bits are tl2[p] / tr2[p].
     float lo2[kMaxM / 2], hi2[kMaxM / 2];
     uint32_t tl2[kMaxM / 2], tr2[kMaxM / 2];
+    float C[kMaxM];
+    float W[kMaxM];    // w2_j * 2^S (fixed-point accumulation scale, see below)
+    float Wn[kMaxM];   // -W_j
     // class of a key for the value grouping in k1_ws: lut[ordered_bits(u) >> 21], 64 classes
     unsigned char lut[2048];
-    // (c, c) pairs of the packed predictor's constants, read from the parameter bank (uniform
-    // registers) instead of occupying vector register pairs: 1, k1, 1.5*2^23
-    unsigned long long one2, k1_2, magic2, pad2;
 };
 
 struct BucketMap {
@@ -111,7 +116,15 @@ __device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
 }
-constexpr uint32_t kSeedNeg = 0xFEF33400u;             // 0x7EF33400 + 0x80000000: bits of -r0 from bits(d)
+constexpr uint32_t kSeedNeg = 0xFEF33400u;
+// Optional exponent shift of the packed predictor: 1/(1 + 2^a) = 2^-s / (2^-s + 2^(a-s)).
+// With s > 0 the chain evaluates d = 2^-s + 2^(a - s) (W scaled by 2^-s), so d stays normal up
+// to a = s + 119 and far fewer warps need the per-activation clamp; but a - s is then rounded
+// at |a - s| ~ s (ulp 2^-17 for s = 100 instead of <= 2^-19), which coarsens y at the steep
+// neurons by about one rank bucket and made K3 slower (0.44 -> 0.58 ms on C2) than K1 got
+// faster (1.044 -> 1.021 ms).  Measured and kept off (s = 0, clamp at 59 -> d <= 2^60).
+constexpr float kAShift = 0.0f;
+constexpr float kAClamp = 60.0f;             // 0x7EF33400 + 0x80000000: bits of -r0 from bits(d)
 
 // Fixed-point accumulation of Eq. 3: every term w2_j * sigma_j is scaled
 // by 2^S (folded into W_j) and rounded to an integer by one FFMA against the magic constant
@@ -138,20 +151,20 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
     for (int q = 0; q < KG; ++q) acc[q] = (int32_t)(0u - (uint32_t)MPAD * (uint32_t)kFxpMagicBits);
     if (PRED == kPredPacked) {
         const f32x2* A2 = reinterpret_cast<const f32x2*>(fw.A);
-        const f32x2* C2 = reinterpret_cast<const f32x2*>(fw.C);
-        const f32x2* Wn2 = reinterpret_cast<const f32x2*>(fw.Wn);
+        const f32x2* C2 = reinterpret_cast<const f32x2*>(fw.Cs);
+        const f32x2* Wn2 = reinterpret_cast<const f32x2*>(fw.Wns);
 #pragma unroll
         for (int j = 0; j < MPAD / 2; ++j) {
 #pragma unroll
             for (int q = 0; q < KG; ++q) {
-                const f32x2 a2 = ffma2(pk2(uh[q], uh[q]), A2[j], C2[j]);
+                const f32x2 a2 = ffma2(pk2(uh[q], uh[q]), A2[j], C2[j]);     // a - s
                 float a0, a1;
                 upk2(a2, a0, a1);
                 if (CLAMP) {
-                    a0 = fminf(a0, 60.0f);           // d = 1 + 2^a stays finite and normal
-                    a1 = fminf(a1, 60.0f);
+                    a0 = fminf(a0, kAClamp);         // d stays finite and normal
+                    a1 = fminf(a1, kAClamp);
                 }
-                const f32x2 d2 = fadd2(pk2(ex2_approx(a0), ex2_approx(a1)), fw.one2);   // d = 1 + e
+                const f32x2 d2 = fadd2(pk2(ex2_approx(a0), ex2_approx(a1)), fw.dofs2);   // d = 2^-s + e
                 float d0, d1;
                 upk2(d2, d0, d1);
                 // the seed's bit trick yields -r0 directly (sign bit folded into the constant)
@@ -160,7 +173,7 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
                 nr2 = fmul2(nr2, ffma2(d2, nr2, fw.k1_2));              // -r1 = -r0 (k1 - d r0)
                 const f32x2 e2 = ffma2(d2, nr2, fw.one2);               // e = 1 - d r1
                 nr2 = ffma2(nr2, ffma2(e2, e2, e2), nr2);               // -r1 (1 + e + e^2)
-                const f32x2 t2 = ffma2(nr2, Wn2[j], fw.magic2);         // W r + magic
+                const f32x2 t2 = ffma2(nr2, Wn2[j], fw.magic2);         // W 2^-s r + magic
                 float t0, t1;
                 upk2(t2, t0, t1);
                 acc[q] = (int32_t)((uint32_t)acc[q] + __float_as_uint(t0) + __float_as_uint(t1));
@@ -205,8 +218,8 @@ __device__ __forceinline__ void gvm_forward_skip(const FoldedWeights& fw, const 
 #pragma unroll
     for (int q = 0; q < KG; ++q) accv[q] = 0u;
     const f32x2* A2 = reinterpret_cast<const f32x2*>(fw.A);
-    const f32x2* C2 = reinterpret_cast<const f32x2*>(fw.C);
-    const f32x2* Wn2 = reinterpret_cast<const f32x2*>(fw.Wn);
+    const f32x2* C2 = reinterpret_cast<const f32x2*>(fw.Cs);
+    const f32x2* Wn2 = reinterpret_cast<const f32x2*>(fw.Wns);
 #pragma unroll 1
     for (int j = 0; j < MPAD / 2; ++j) {
         if (umax < fw.lo2[j]) {
@@ -224,10 +237,10 @@ __device__ __forceinline__ void gvm_forward_skip(const FoldedWeights& fw, const 
             float a0, a1;
             upk2(a2, a0, a1);
             if (CLAMP) {
-                a0 = fminf(a0, 60.0f);
-                a1 = fminf(a1, 60.0f);
+                a0 = fminf(a0, kAClamp);
+                a1 = fminf(a1, kAClamp);
             }
-            const f32x2 d2 = fadd2(pk2(ex2_approx(a0), ex2_approx(a1)), fw.one2);
+            const f32x2 d2 = fadd2(pk2(ex2_approx(a0), ex2_approx(a1)), fw.dofs2);
             float d0, d1;
             upk2(d2, d0, d1);
             f32x2 nr2 = pk2(__uint_as_float(kSeedNeg - __float_as_uint(d0)),

@@ -99,7 +99,7 @@ int main() {
         kp.num_tiles = (uint32_t)((n + T - 1) / T);
         const size_t sm = k1ws_smem_bytes(4, T, C);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        const float ms = time_kernel([&] { kern<<<148, kWsThreads, sm>>>(keys, fw, kp, rk, rf, nullptr, cursor, st); },
+        const float ms = time_kernel([&] { kern<<<148, ws_threads(false), sm>>>(keys, kp, rk, rf, nullptr, cursor, st, nullptr, fw); },
                                      cursor, C, 5);
         cudaError_t e = cudaGetLastError();
         printf("%-40s %8.3f ms  %6.2f act/clk/SM @1965  (%s)\n", name, ms, acts / (ms * 1e-3) / 148 / 1.965e9,
