@@ -66,7 +66,7 @@ struct K3LParams {
 __host__ __device__ inline uint32_t k3l_hist_words(uint32_t kfine) { return ((kfine + 1u) / 2u + 3u) & ~3u; }
 
 constexpr uint32_t kL3WarpQ = 64;       // per-warp fix-up queue entries (power of two)
-__host__ __device__ constexpr size_t k3l_queue_bytes(int nt) { return (size_t)(nt / 32) * kL3WarpQ * 4; }
+__host__ __device__ constexpr size_t k3l_queue_bytes(int nt) { return (size_t)(nt / 32) * 2 * kL3WarpQ * 4; }
 
 // smem: ctrl | per-warp fix-up queues | hist (u16 pairs) | skey[cap] | sidx[cap] (perm)
 inline size_t k3l_smem_bytes(size_t ks, bool perm, uint32_t kfine, uint32_t cap, int nt) {
@@ -457,14 +457,14 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         K3L_T(3);
         // ---- 4. fix-up in place ("only the numbers inside each bucket need to be sorted").
         // Warp v walks 32 counter words (64 rank buckets) per batch.  Buckets of 0-1 elements
-        // (~70 % of them) need nothing; those of 2-4 are compacted into a per-warp queue (ballot +
-        // prefix) and sorted 32 at a time, one per lane, by a padded 4-element network in
-        // registers; 5..8 elements (rare) by an 8-element network and up to kL3RankMax by insertion
-        // in their own lane, longer ones
+        // (~70 % of them) need nothing; those of 2-4 and of 5-8 are compacted into two per-warp
+        // queues (ballot + prefix) and sorted 32 at a time, one per lane, by padded 4- and
+        // 8-element networks in registers; up to kL3RankMax by insertion in their own lane, longer ones
         // (tails clamped into the end buckets, heavy duplicates) queued for a block-wide sort.
         {
-            uint32_t* wq = wqueue + warp * kL3WarpQ;
-            uint32_t qn = 0, qd = 0;                   // warp-uniform: entries queued / sorted
+            uint32_t* wq = wqueue + warp * 2 * kL3WarpQ;        // 2..4-element buckets
+            uint32_t* wq8 = wq + kL3WarpQ;                      // 5..8-element buckets
+            uint32_t qn = 0, qd = 0, qn8 = 0, qd8 = 0;          // warp-uniform: queued / sorted
             const uint32_t lt = (1u << lane) - 1u;
             for (uint32_t wb = (uint32_t)warp * 32u; wb < hw; wb += NT) {
                 const uint32_t w = wb + lane;
@@ -478,10 +478,8 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
                 }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    if (len[h] > 4u) {                 // rare: sorted by their own lane
-                        if (len[h] <= 8u) {
-                            k3l_sortn<KeyT, PERM, 8>(skey, sidx, sb[h], len[h]);
-                        } else if (len[h] <= kL3RankMax) {
+                    if (len[h] > 8u) {                          // rare: by their own lane / block
+                        if (len[h] <= kL3RankMax) {
                             k3l_insertion<KeyT, PERM>(skey, sidx, sb[h], sb[h] + len[h]);
                         } else {
                             const uint32_t q = atomicAdd(&ctrl[2], 1u);
@@ -491,22 +489,39 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
                             }
                         }
                     }
+                    const uint32_t ent = sb[h] | (len[h] << 16);
                     const bool need = len[h] - 2u <= 2u;
                     const uint32_t m = __ballot_sync(0xffffffffu, need);
-                    if (need) wq[(qn + __popc(m & lt)) & (kL3WarpQ - 1u)] = sb[h] | (len[h] << 16);
+                    if (need) wq[(qn + __popc(m & lt)) & (kL3WarpQ - 1u)] = ent;
                     qn += __popc(m);
+                    const bool need8 = len[h] - 5u <= 3u;
+                    const uint32_t m8 = __ballot_sync(0xffffffffu, need8);
+                    if (m8) {
+                        if (need8) wq8[(qn8 + __popc(m8 & lt)) & (kL3WarpQ - 1u)] = ent;
+                        qn8 += __popc(m8);
+                    }
                     __syncwarp();
                     if (qn - qd >= 32u) {
-                        const uint32_t ent = wq[(qd + lane) & (kL3WarpQ - 1u)];
-                        k3l_sortn<KeyT, PERM, 4>(skey, sidx, ent & 0xffffu, ent >> 16);
+                        const uint32_t e = wq[(qd + lane) & (kL3WarpQ - 1u)];
+                        k3l_sortn<KeyT, PERM, 4>(skey, sidx, e & 0xffffu, e >> 16);
                         qd += 32u;
+                        __syncwarp();
+                    }
+                    if (qn8 - qd8 >= 32u) {
+                        const uint32_t e = wq8[(qd8 + lane) & (kL3WarpQ - 1u)];
+                        k3l_sortn<KeyT, PERM, 8>(skey, sidx, e & 0xffffu, e >> 16);
+                        qd8 += 32u;
                         __syncwarp();
                     }
                 }
             }
             if (lane < qn - qd) {
-                const uint32_t ent = wq[(qd + lane) & (kL3WarpQ - 1u)];
-                k3l_sortn<KeyT, PERM, 4>(skey, sidx, ent & 0xffffu, ent >> 16);
+                const uint32_t e = wq[(qd + lane) & (kL3WarpQ - 1u)];
+                k3l_sortn<KeyT, PERM, 4>(skey, sidx, e & 0xffffu, e >> 16);
+            }
+            if (lane < qn8 - qd8) {
+                const uint32_t e = wq8[(qd8 + lane) & (kL3WarpQ - 1u)];
+                k3l_sortn<KeyT, PERM, 8>(skey, sidx, e & 0xffffu, e >> 16);
             }
         }
         __syncthreads();

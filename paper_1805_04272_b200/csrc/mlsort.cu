@@ -352,7 +352,7 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
         p.k3_smem = k3l_smem_bytes(ks, perm, kfine, (uint32_t)cap, kL3ThreadsBig);
         // two-CTA primary pass only when it holds the average bucket with margin
         p.cap1 = k3l_cap_for(kK3LSmemPrimary, ks, perm, kfine, kL3Threads);
-        if ((double)p.cap1 < 1.15 * avg + 64.0) p.cap1 = 0;
+        if ((double)p.cap1 < 1.1 * avg + 64.0) p.cap1 = 0;
         p.k3_smem1 = p.cap1 ? k3l_smem_bytes(ks, perm, kfine, p.cap1, kL3Threads) : 0;
         uint64_t cc = (uint64_t)std::ceil(kRegionFactor * avg) + 64;
         cc = (cc + 7) & ~7ull;
