@@ -49,6 +49,7 @@ constexpr int kL3Threads = 512;         // primary pass: two CTAs per SM
 constexpr int kL3ThreadsBig = 1024;     // secondary pass (larger coarse buckets): one CTA per SM
 constexpr uint32_t kL3RankMax = 24;     // rank buckets up to this size: insertion sort by one thread
 constexpr uint32_t kL3BigQ = 48;        // queued larger rank buckets per coarse bucket
+constexpr int kL3FineRegs = 5;          // 128-bit vectors of fine ids kept in registers per thread
 
 struct K3LParams {
     uint32_t capc;          // region capacity (elements) per coarse bucket
@@ -364,16 +365,19 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         // ---- 1. histogram of rank buckets (8 ids per 128-bit load; rows are 16-B aligned)
         for (uint32_t w = tid; w < hwp; w += NT) h2[w] = 0u;
         __syncthreads();
-        {
-            uint32_t i = tid;
-            for (; i + NT < n8; i += 2 * NT) {                    // two loads in flight
-                const uint4 v = __ldg(g8 + i), w = __ldg(g8 + i + NT);
-                hist_add8(h2, v);
-                hist_add8(h2, w);
-            }
-            if (i < n8) hist_add8(h2, __ldg(g8 + i));
-            for (uint32_t q = (n8 << 3) + tid; q < n; q += NT) hist_inc(h2, gf[q]);
+        // the first kL3FineRegs 128-bit vectors of fine ids per thread stay in registers for the
+        // placement (a second read of them from L2 missed to DRAM: ncu v7 read 1.34x the bytes)
+        uint4 fr[kL3FineRegs];
+#pragma unroll
+        for (int k = 0; k < kL3FineRegs; ++k) {
+            const uint32_t i = tid + k * NT;
+            fr[k] = i < n8 ? __ldg(g8 + i) : make_uint4(0u, 0u, 0u, 0u);
         }
+#pragma unroll
+        for (int k = 0; k < kL3FineRegs; ++k)
+            if (tid + k * NT < n8) hist_add8(h2, fr[k]);
+        for (uint32_t i = tid + kL3FineRegs * NT; i < n8; i += NT) hist_add8(h2, __ldg(g8 + i));
+        for (uint32_t q = (n8 << 3) + tid; q < n; q += NT) hist_inc(h2, gf[q]);
         __syncthreads();
         K3L_T(1);
         // ---- 2. exclusive scan of the counters: thread t scans its own WPT consecutive words
@@ -427,8 +431,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         __syncthreads();
         K3L_T(2);
         // ---- 3. placement into rank-bucket order (ids + keys as 128-bit vectors)
-        for (uint32_t i = tid; i < n8; i += NT) {
-            const uint4 fv = __ldg(g8 + i);
+        auto place8 = [&](uint32_t i, const uint4 fv) {
             KeyT kv[8];
             load8<KeyT>(gk + 8 * (size_t)i, kv);
             uint32_t iv[8];
@@ -446,7 +449,11 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
                 skey[pos] = KeyTraits<KeyT>::to_ord(kv[k]);
                 if (PERM) sidx[pos] = iv[k];
             }
-        }
+        };
+#pragma unroll
+        for (int k = 0; k < kL3FineRegs; ++k)
+            if (tid + k * NT < n8) place8(tid + k * NT, fr[k]);
+        for (uint32_t i = tid + kL3FineRegs * NT; i < n8; i += NT) place8(i, __ldg(g8 + i));
         for (uint32_t q = (n8 << 3) + tid; q < n; q += NT) {
             const uint32_t f = gf[q];
             const uint32_t pos = hist_inc_ret(h2, f);
