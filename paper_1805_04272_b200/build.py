@@ -42,6 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if src.endswith(".cu"):
             cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                    "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+            cmd += os.environ.get("MLSORT_NVCC_FLAGS", "").split()     # experiments only (-D...)
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
         else:

@@ -510,12 +510,17 @@ cudaError_t launch_k1_t(const Plan& p, const KeyT* keys, const FoldedWeights& fw
     return cudaGetLastError();
 }
 
+#ifndef MLSORT_K1_KG
+#define MLSORT_K1_KG 8
+#endif
+constexpr int kK1Kg = MLSORT_K1_KG;   // keys per predictor lane in flight (k1_ws KGW)
+
 template <typename KeyT, int MPAD, int PRED, bool PERM>
 cudaError_t launch_k1_ws_t(const Plan& p, const KeyT* keys, const FoldedWeights& fw, const K1Params& kp, void* ws,
                            const Layout& L, cudaStream_t s, const unsigned long long* rbase) {
     const bool group = PRED == kPredPacked && p.ws_group;
     auto kern = group ? k1_ws<KeyT, MPAD, PRED, PERM, 8, true, PRED == kPredPacked>
-                      : k1_ws<KeyT, MPAD, PRED, PERM, 8, true, false>;
+                      : k1_ws<KeyT, MPAD, PRED, PERM, kK1Kg, true, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k1_smem);
     if (e != cudaSuccess) return e;
     const int grid = std::min<int>(num_sms(), (int)kp.num_tiles);
