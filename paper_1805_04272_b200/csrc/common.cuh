@@ -113,4 +113,19 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// bulk L2 prefetch of [p, p + bytes) (cp.async.bulk.prefetch.L2; 16-B granularity)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    // bulk L2 prefetch: 16-B aligned address and size
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uintptr_t a0 = a & ~(uintptr_t)15;
+    uint32_t sz = (uint32_t)(((a + bytes + 15) & ~(uintptr_t)15) - a0);
+    const char* q = reinterpret_cast<const char*>(a0);
+    while (sz) {
+        const uint32_t chunk = sz > 65536u ? 65536u : sz;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(chunk) : "memory");
+        q += chunk;
+        sz -= chunk;
+    }
+}
+
 }  // namespace mlsort

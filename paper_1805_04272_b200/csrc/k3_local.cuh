@@ -85,20 +85,6 @@ inline uint32_t k3l_cap_for(size_t budget, size_t ks, bool perm, uint32_t kfine,
     return (uint32_t)cap;
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    // bulk L2 prefetch: 16-B aligned address and size
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    const uintptr_t a0 = a & ~(uintptr_t)15;
-    uint32_t sz = (uint32_t)(((a + bytes + 15) & ~(uintptr_t)15) - a0);
-    const char* q = reinterpret_cast<const char*>(a0);
-    while (sz) {
-        const uint32_t chunk = sz > 65536u ? 65536u : sz;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(chunk) : "memory");
-        q += chunk;
-        sz -= chunk;
-    }
-}
-
 template <typename KeyT, bool PERM>
 __device__ __forceinline__ void prefetch_bucket(const KeyT* reg_keys, const uint16_t* reg_fine, const uint32_t* reg_idx,
                                                 size_t rb, unsigned long long n) {
