@@ -217,9 +217,33 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
 // Global starts of the coarse buckets: exclusive scan of the exact bucket sizes (the final
 // region cursors), one CTA.  starts[C] = n.
 __global__ void __launch_bounds__(1024)
-k2_coarse_starts(const uint32_t* __restrict__ cursor, uint32_t C, unsigned long long* __restrict__ starts) {
+k2_coarse_starts(const uint32_t* __restrict__ cursor, uint32_t C, unsigned long long* __restrict__ starts,
+                 bool one_pass) {
     __shared__ uint32_t scratch[64];
     __shared__ unsigned long long carry;
+    const uint32_t k = (C + 1023u) / 1024u;              // counts per thread
+    if (one_pass && k <= 16u) {                          // (one_pass: the total fits 32 bits)
+        // one pass: every thread loads its k consecutive counts at once (one memory latency),
+        // one block scan of the per-thread sums, then the k starts
+        const uint32_t c0 = threadIdx.x * k;
+        uint32_t v[16], tot = 0;
+#pragma unroll
+        for (uint32_t q = 0; q < 16; ++q) {
+            v[q] = (q < k && c0 + q < C) ? cursor[c0 + q] : 0u;
+            tot += v[q];
+        }
+        uint32_t all;
+        unsigned long long run = block_exclusive_scan<1024>(tot, scratch, &all);
+#pragma unroll
+        for (uint32_t q = 0; q < 16; ++q) {
+            if (q < k && c0 + q < C) {
+                starts[c0 + q] = run;
+                run += v[q];
+            }
+        }
+        if (threadIdx.x == 0) starts[C] = all;
+        return;
+    }
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     for (uint32_t b0 = 0; b0 < C; b0 += 1024) {

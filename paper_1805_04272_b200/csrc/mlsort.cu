@@ -868,7 +868,8 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
             CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kp, ws, L, s, bucket_in, idx_in, b_lo, rbase)));
         }
         tm.mark();
-        k2_coarse_starts<<<1, 1024, 0, s>>>(at<uint32_t>(ws, L.cursor), p.C, at<unsigned long long>(ws, L.starts));
+        k2_coarse_starts<<<1, 1024, 0, s>>>(at<uint32_t>(ws, L.cursor), p.C, at<unsigned long long>(ws, L.starts),
+                                            n < (1ull << 31));
         CK(cudaGetLastError());
         tm.mark();
         // Rank-bucket-level verification (reading A14) is needed only when the network is not
