@@ -757,6 +757,9 @@ K1Params k1_params(const Weights& w, const Plan& p, uint64_t B, bool f32) {
     kp.bm.Bm1 = (uint32_t)(B - 1);
     kp.bm.B = B;
     kp.bm.S = fxp_shift(w);
+    kp.bm.pow2 = (B & (B - 1)) == 0 && B <= (1ull << 32) ? 1u : 0u;
+    kp.bm.sh = (int32_t)kp.bm.S - (int32_t)ceil_log2(B);
+    kp.bm.half = kp.bm.sh > 0 ? (1 << (kp.bm.sh - 1)) : 0;
     kp.fine_bits = p.fb;
     kp.num_coarse = p.C;
     kp.num_tiles = p.T;

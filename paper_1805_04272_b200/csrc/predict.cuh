@@ -53,6 +53,8 @@ struct BucketMap {
     uint32_t Bm1;      // B - 1
     unsigned long long B;
     uint32_t S;        // y = acc * 2^-S
+    uint32_t pow2;     // B = 2^k: the bucket is a shift of acc (sh = S - k, half = 2^(sh-1) or 0)
+    int32_t sh, half;
 };
 
 __device__ __forceinline__ float ex2_approx(float a) {
@@ -268,6 +270,13 @@ __device__ __forceinline__ uint32_t f32_ordbits(float x) {
 // (S:232, S:297-S:298).  For y >= 0 round-half-up equals round-half-away-
 // from-zero (reading A6); negative y map to bucket 0.
 __device__ __forceinline__ uint32_t bucket_of_fxp(int32_t acc, const BucketMap& bm) {
+    if (bm.pow2) {
+        // B = 2^k: (acc * 2^k + 2^(S-1)) >> S == (acc + 2^(sh-1)) >> sh for sh = S - k > 0,
+        // == acc for sh = 0 and == acc * 2^-sh for sh < 0 (the 1/2 floors away), exactly
+        long long r = bm.sh >= 0 ? (long long)((acc + bm.half) >> bm.sh) : (long long)acc << (-bm.sh);
+        r = r < 0 ? 0 : r;
+        return r < (long long)bm.Bm1 ? (uint32_t)r : bm.Bm1;
+    }
     const long long v = (long long)acc * (long long)bm.B + (1ll << (bm.S - 1));
     if (v < 0) return 0u;
     const unsigned long long r = (unsigned long long)v >> bm.S;
