@@ -49,7 +49,10 @@ constexpr int kL3Threads = 512;         // primary pass: two CTAs per SM
 constexpr int kL3ThreadsBig = 1024;     // secondary pass (larger coarse buckets): one CTA per SM
 constexpr uint32_t kL3RankMax = 24;     // rank buckets up to this size: insertion sort by one thread
 constexpr uint32_t kL3BigQ = 48;        // queued larger rank buckets per coarse bucket
-constexpr int kL3FineRegs = 5;          // 128-bit vectors of fine ids kept in registers per thread
+constexpr int kL3FineRegs = 5;
+#ifndef MLSORT_K3_LATE_PF
+#define MLSORT_K3_LATE_PF 0     // 1: prefetch the next bucket after the scan instead of at the ticket
+#endif          // 128-bit vectors of fine ids kept in registers per thread
 
 struct K3LParams {
     uint32_t capc;          // region capacity (elements) per coarse bucket
@@ -247,7 +250,7 @@ __device__ __forceinline__ void k3l_store(const typename K3Out<T>::Bits* src, ui
                 const T t = K3Out<T>::conv(sp[4 * v + c]);
                 qq[c] = *reinterpret_cast<const uint32_t*>(&t);
             }
-            reinterpret_cast<float4*>(o)[v] = q;
+            __stcs(reinterpret_cast<float4*>(o) + v, q);     // streaming: keep L2 for the regions
         } else {
             double2 q;
             unsigned long long* qq = reinterpret_cast<unsigned long long*>(&q);
@@ -256,7 +259,7 @@ __device__ __forceinline__ void k3l_store(const typename K3Out<T>::Bits* src, ui
                 const T t = K3Out<T>::conv(sp[2 * v + c]);
                 qq[c] = *reinterpret_cast<const unsigned long long*>(&t);
             }
-            reinterpret_cast<double2*>(o)[v] = q;
+            __stcs(reinterpret_cast<double2*>(o) + v, q);
         }
     }
     for (uint32_t i = head + nv * V + threadIdx.x; i < n; i += NT) out[i] = K3Out<T>::conv(src[i]);
@@ -314,17 +317,32 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             const uint32_t t1 = (uint32_t)atomicAdd(ticket, 1ull);
             ctrl[1] = t1;
             ctrl[2] = 0;
+#if !MLSORT_K3_LATE_PF
             if (t1 < items) {
                 const uint32_t c1 = coarse_of(t1);
                 const unsigned long long s1 = starts[c1], n1 = starts[c1 + 1] - s1;
                 if (n1 <= p.cap) prefetch_bucket<KeyT, PERM>(reg_keys, reg_fine, reg_idx, region_base(rbase, c1, p.capc), n1);
             }
+#endif
         }
+        // the next bucket's region is asked into L2 after this bucket's scan (step 2), about
+        // half a bucket ahead of its use: an earlier prefetch was partly evicted before use
+        auto prefetch_next = [&]() {
+            if (!MLSORT_K3_LATE_PF || tid != 0) return;
+            const uint32_t t1 = ctrl[1];
+            if (t1 < items) {
+                const uint32_t c1 = coarse_of(t1);
+                const unsigned long long s1 = starts[c1], n1 = starts[c1 + 1] - s1;
+                if (n1 <= p.cap) prefetch_bucket<KeyT, PERM>(reg_keys, reg_fine, reg_idx, region_base(rbase, c1, p.capc), n1);
+            }
+        };
         if (n == 0) {
+            prefetch_next();
             if (tid == 0) range_start[c] = ~0ull;
             continue;
         }
         if (n > p.cap) {                       // too large for this pass
+            prefetch_next();
             if (tid == 0) {
                 atomicMax(&st->max_coarse, (unsigned long long)n);
                 if (p.to_mid) {
@@ -415,6 +433,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             }
         }
         __syncthreads();
+        prefetch_next();
         K3L_T(2);
         // ---- 3. placement into rank-bucket order (ids + keys as 128-bit vectors)
         auto place8 = [&](uint32_t i, const uint4 fv) {
