@@ -22,7 +22,13 @@
 
 namespace mlsort {
 
-constexpr int kPartWarps = 8;
+#ifndef MLSORT_K1_PARTW
+#define MLSORT_K1_PARTW 8
+#endif
+#ifndef MLSORT_K1_PREDW
+#define MLSORT_K1_PREDW 24
+#endif
+constexpr int kPartWarps = MLSORT_K1_PARTW;   // (macros: warp-split experiments)
 constexpr int kPartThreads = kPartWarps * 32;     // 256
 constexpr int kClasses = 64;
 
@@ -31,7 +37,7 @@ constexpr int kClasses = 64;
 // which leaves room for the tile's u values in class order.
 template <typename KeyT, bool GROUP>
 struct WsCfg {
-    static constexpr int kPredWarps = GROUP ? 16 : 24;
+    static constexpr int kPredWarps = GROUP ? 16 : MLSORT_K1_PREDW;
     static constexpr int kThreads = (kPredWarps + kPartWarps) * 32;
     static constexpr int kPredThreads = kPredWarps * 32;
     static constexpr int kKPT = sizeof(KeyT) == 4 ? 16 : 8;   // keys per predictor thread per tile
