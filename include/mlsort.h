@@ -54,12 +54,17 @@ typedef enum { MLSORT_F32 = 0, MLSORT_F64 = 1 } mlsort_dtype;
 /* Which f32 formulation of the logistic the predict kernel uses.
  * All meet |y - y_fp64| <= 1e-5; the output sort is bit-exact for every choice. */
 typedef enum {
-    MLSORT_PRED_DEFAULT = 0,   /* library choice (currently MLSORT_PRED_PACKED)                */
+    MLSORT_PRED_DEFAULT = 0,   /* library choice: MLSORT_PRED_PACKED for M <= 32,
+                                  MLSORT_PRED_SKIP for M > 32                                  */
     MLSORT_PRED_MUFU = 1,      /* ex2 + rcp both on the SFU: 2 MUFU per activation             */
     MLSORT_PRED_MIXED = 2,     /* ex2 on the SFU; reciprocal split between SFU and scalar
                                   FMA-pipe Newton iterations                                   */
-    MLSORT_PRED_PACKED = 3     /* ex2 on the SFU; reciprocal on the FMA pipe with packed f32x2
+    MLSORT_PRED_PACKED = 3,    /* ex2 on the SFU; reciprocal on the FMA pipe with packed f32x2
                                   instructions (bit-trick seed, modified Newton + cubic step)  */
+    MLSORT_PRED_SKIP = 4       /* MLSORT_PRED_PACKED arithmetic, skipping neuron pairs that are
+                                  saturated over a warp's key range (their terms are exact
+                                  constants): bit-identical outputs; the sort groups each tile
+                                  by value first so warps span narrow ranges                    */
 } mlsort_predictor;
 
 /* Opaque host-resident GVM parameters {m, w1, w2, b, beta, input_lo, input_hi}
@@ -69,9 +74,9 @@ typedef struct mlsort_weights mlsort_weights;
 typedef struct {
     uint64_t num_buckets;   /* B, the number of rank buckets; 0 means B = n          */
     int32_t  predictor;     /* mlsort_predictor                                             */
-    int32_t  verify;        /* 0/1 (default): every coarse-bucket boundary is verified (K5),
-                               rank-bucket boundaries only when the weights are not
-                               sign-feasible (Eq. 4); 2: verify every rank-bucket boundary  */
+    int32_t  verify;        /* accepted for compatibility, no effect: the adjacent order of
+                               every output pair is always verified (K3 inside each coarse
+                               bucket, K5 at coarse boundaries; reading A14)          */
     int32_t  timing;        /* 1 = record CUDA events around each kernel phase and report
                                the device times in mlsort_info.phase_ms (bench/profiling)     */
     int32_t  reserved[3];   /* must be zero                                                 */
@@ -196,6 +201,23 @@ int mlsort_sort_host(const void* h_keys, uint64_t n, mlsort_dtype dtype,
 int mlsort_predict(const void* d_keys, uint64_t n, mlsort_dtype dtype, const mlsort_weights* w,
                    uint64_t num_buckets, int32_t predictor, float* d_y, uint32_t* d_bucket,
                    void* stream);
+
+/* Diagnostic (reading A14; SURVEY.md §8(c) "exhaustive monotonicity", K8).  PAPER.md Eq. 4
+ * (l.76-84) makes the network monotone in exact arithmetic; the f32 device predictor is
+ * monotone if the approximate primitives it is built from are.  This evaluates one of them
+ * on EVERY input of its domain, in ascending order, on the current device:
+ *   0 ex2.approx.ftz.f32 over all non-NaN f32 (must be non-decreasing),
+ *   1 the packed FMA-pipe reciprocal chain over every f32 d in [1, 2^61] (non-increasing;
+ *     *max_rel_err = max |r d - 1|),
+ *   2 rcp.approx.ftz.f32 over every positive f32 (non-increasing),
+ *   3 the packed predictor's logistic term 1/(1 + ex2(min(a, 60))) over all non-NaN a
+ *     (non-increasing).
+ * *descents = adjacent input pairs whose outputs go the wrong way (0 = monotone);
+ * *evaluated = inputs evaluated.  Any output pointer may be NULL.  Synchronises `stream`.
+ * Sort correctness never depends on the result (every adjacent output pair is verified);
+ * a descent would only cost repairs.  Errors: MLSORT_ERR_INVALID_ARG, MLSORT_ERR_CUDA. */
+int mlsort_selftest_monotone(int32_t primitive, uint64_t* descents, uint64_t* evaluated,
+                             double* max_rel_err, void* stream);
 
 /* ------------------------------------------------------------------ multi-GPU building blocks
  * One process per GPU.  Rank g holds the contiguous input slice

@@ -218,11 +218,38 @@ def order_bits(keys) -> np.ndarray:
     return np.where(u >> 63, ~u, u | np.uint64(0x8000000000000000)).astype(np.uint64)
 
 
-def sorted_reference(keys):
-    """(sorted keys, perm) = stable sort of (key, index) under totalOrder."""
+def sorted_reference(keys, want_perm: bool = True):
+    """(sorted keys, perm or None) = stable sort of (key, index) under totalOrder.
+
+    The stable order is the order of the pairs (order_bits(key), index), and these pairs are
+    distinct, so sorting them with any sort gives it.  For f32 keys a pair fits one uint64
+    (order bits << 32 | index, n < 2^32) and numpy's plain np.sort orders them; for f64 keys
+    with a permutation np.argsort(kind="stable") of the order bits; for key-only output the
+    order bits alone (equal bits are equal keys).  Pinned against brute-force ranks and
+    np.argsort(kind="stable") in tests/test_oracle_pins.py."""
+    keys = np.asarray(keys)
     ob = order_bits(keys)
+    n = ob.shape[0]
+    if not want_perm:
+        sb = np.sort(ob)
+        return _from_order_bits(sb, keys.dtype), None
+    if keys.dtype == np.float32 and n < (1 << 32):
+        pair = (ob.astype(np.uint64) << np.uint64(32)) | np.arange(n, dtype=np.uint64)
+        pair.sort()
+        perm = (pair & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+        sk = _from_order_bits((pair >> np.uint64(32)).astype(np.uint32), keys.dtype)
+        return sk, perm
     perm = np.argsort(ob, kind="stable").astype(np.uint32)
-    return np.asarray(keys)[perm], perm
+    return keys[perm], perm
+
+
+def _from_order_bits(ob, dtype):
+    """Inverse of order_bits."""
+    if dtype == np.float32:
+        u = np.where(ob >> np.uint32(31), ob & np.uint32(0x7FFFFFFF), ~ob).astype(np.uint32)
+        return u.view(np.float32)
+    u = np.where(ob >> np.uint64(63), ob & np.uint64(0x7FFFFFFFFFFFFFFF), ~ob).astype(np.uint64)
+    return u.view(np.float64)
 
 
 def select_sorted(keys, positions, stable: bool = True):

@@ -23,7 +23,7 @@ _LIB_PATH = os.path.join(_HERE, "libmlsort.so")
 _lib = None
 
 F32, F64 = 0, 1
-PRED_DEFAULT, PRED_MUFU, PRED_MIXED, PRED_PACKED = 0, 1, 2, 3
+PRED_DEFAULT, PRED_MUFU, PRED_MIXED, PRED_PACKED, PRED_SKIP = 0, 1, 2, 3, 4
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "I/O error", 3: "weights JSON parse error",
           4: "invalid weights", 5: "non-finite key", 6: "CUDA error", 7: "workspace",
@@ -101,6 +101,7 @@ def lib():
                                             P, C.POINTER(Info)]
         L.mlsort_sort_records_workspace_size.argtypes = [u64, i32, u64, u64, C.POINTER(u64)]
         L.mlsort_sort_records.argtypes = [P, P, P, u64, i32, u64, u64, P, P, P, u64, P, C.POINTER(Info)]
+        L.mlsort_selftest_monotone.argtypes = [i32, C.POINTER(u64), C.POINTER(u64), C.POINTER(d), P]
         _lib = L
     return _lib
 
@@ -400,6 +401,19 @@ def sort_records(keys, bucket, index, bucket_lo: int, bucket_hi: int, stream=Non
                                    C.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream), C.byref(info))
     _check(rc, "mlsort_sort_records", info)
     return out_k, out_i, info.as_dict()
+
+
+SWEEP_EX2, SWEEP_RCP_CHAIN, SWEEP_RCP_MUFU, SWEEP_LOGISTIC = 0, 1, 2, 3
+
+
+def selftest_monotone(primitive: int, stream=None) -> dict:
+    """K8 primitive sweep on the current device (mlsort_selftest_monotone): evaluates one of
+    the predictor's approximate primitives on every input of its domain in ascending order.
+    Returns {"descents", "evaluated", "max_rel_err"}."""
+    desc, ev, rel = C.c_uint64(), C.c_uint64(), C.c_double()
+    _check(lib().mlsort_selftest_monotone(primitive, C.byref(desc), C.byref(ev), C.byref(rel), _stream_ptr(stream)),
+           "mlsort_selftest_monotone")
+    return {"descents": desc.value, "evaluated": ev.value, "max_rel_err": rel.value}
 
 
 def version() -> str:

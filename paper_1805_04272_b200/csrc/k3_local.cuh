@@ -8,11 +8,10 @@
 //   2. exclusive scan -> start of every rank bucket                                  -- A4
 //   3. placement: every key goes to start[f]++ in shared memory (order-preserving
 //      unsigned key bits; index alongside for perm sorts)                            -- A5
-//   4. fix-up fused with the store: every position ranks its element inside its rank bucket
-//      by counting the bucket's elements that precede it under (totalOrder key, input index)
-//      and writes it to its final position; large buckets get a block bitonic sort     -- A6
-//   5. when the weights are not provably monotone: the stored output is checked at every
-//      rank-bucket boundary and an inversion re-sorts the whole coarse bucket    -- A7 (A14)
+//   4. fix-up in place: rank buckets of 2-8 elements by register sorting networks, up to 24 by
+//      insertion, larger ones by a block bitonic sort                                  -- A6
+//   5. the store is fused with an adjacent-order check of the whole coarse bucket; an
+//      inversion (non-monotone model or float effects) re-sorts it in smem  -- A7 (A14)
 // The primary pass runs two 512-thread CTAs per SM (two coarse buckets in flight hide each
 // other's phase latencies) with a capacity of ~1.3x the average coarse bucket; larger buckets
 // go to a secondary pass of one 1024-thread CTA per SM with the whole 227 KB, and only
@@ -59,7 +58,6 @@ struct K3LParams {
     uint32_t num_coarse;    // C
     uint32_t kfine;         // rank buckets per coarse bucket (2^fine_bits)
     uint32_t cap;           // largest coarse bucket this pass holds in shared memory
-    uint32_t verify;        // 1: check every rank-bucket boundary (weights not provably monotone)
     uint32_t secondary;     // 0: pass over all coarse buckets; 1: pass over mid_list
     uint32_t to_mid;        // too-large buckets go to mid_list (1, primary of two passes) or to
                             // K4's big_list (0)
@@ -263,6 +261,74 @@ __device__ __forceinline__ void k3l_store(const typename K3Out<T>::Bits* src, ui
         }
     }
     for (uint32_t i = head + nv * V + threadIdx.x; i < n; i += NT) out[i] = K3Out<T>::conv(src[i]);
+}
+
+// k3l_store of the keys fused with the order check of reading A14: every thread also compares
+// each element it stores with its predecessor, (key, index) strictly increasing for perm sorts
+// (indices are distinct), keys non-decreasing otherwise.  Returns this thread's "inversion seen".
+template <typename KeyT, bool PERM, int NT>
+__device__ __forceinline__ bool k3l_store_verify(const typename KeyTraits<KeyT>::Bits* src, const uint32_t* sidx,
+                                                 uint32_t n, KeyT* out) {
+    using Bits = typename KeyTraits<KeyT>::Bits;
+    constexpr uint32_t V = 16 / sizeof(KeyT);
+    bool bad = false;
+    auto chk = [&](uint32_t i, Bits cur) {
+        if (i == 0) return;
+        const Bits prev = src[i - 1];
+        bad |= PERM ? !precedes<KeyT, true>(prev, sidx[i - 1], cur, sidx[i]) : cur < prev;
+    };
+    const uint32_t head = min(n, (uint32_t)(((16u - ((uint32_t)reinterpret_cast<uintptr_t>(out) & 15u)) & 15u) / sizeof(KeyT)));
+    if (threadIdx.x < head) {
+        const Bits c = src[threadIdx.x];
+        chk(threadIdx.x, c);
+        out[threadIdx.x] = K3Out<KeyT>::conv(c);
+    }
+    const uint32_t nv = (n - head) / V;
+    KeyT* o = out + head;
+    for (uint32_t v = threadIdx.x; v < nv; v += NT) {
+        const uint32_t i0 = head + V * v;
+        Bits c[V];
+#pragma unroll
+        for (uint32_t q = 0; q < V; ++q) c[q] = src[i0 + q];
+        Bits prev = i0 ? src[i0 - 1] : c[0];
+        uint32_t pi = (PERM && i0) ? sidx[i0 - 1] : 0u;
+#pragma unroll
+        for (uint32_t q = 0; q < V; ++q) {
+            if (PERM) {
+                const uint32_t ci = sidx[i0 + q];
+                if (i0 + q) bad |= !(prev < c[q] || (prev == c[q] && pi < ci));
+                pi = ci;
+            } else {
+                bad |= c[q] < prev;
+            }
+            prev = c[q];
+        }
+        if (V == 4) {
+            float4 qv;
+            uint32_t* qq = reinterpret_cast<uint32_t*>(&qv);
+#pragma unroll
+            for (uint32_t q = 0; q < V; ++q) {
+                const KeyT t = K3Out<KeyT>::conv(c[q]);
+                qq[q] = *reinterpret_cast<const uint32_t*>(&t);
+            }
+            __stcs(reinterpret_cast<float4*>(o) + v, qv);
+        } else {
+            double2 qv;
+            unsigned long long* qq = reinterpret_cast<unsigned long long*>(&qv);
+#pragma unroll
+            for (uint32_t q = 0; q < V; ++q) {
+                const KeyT t = K3Out<KeyT>::conv(c[q]);
+                qq[q] = *reinterpret_cast<const unsigned long long*>(&t);
+            }
+            __stcs(reinterpret_cast<double2*>(o) + v, qv);
+        }
+    }
+    for (uint32_t i = head + nv * V + threadIdx.x; i < n; i += NT) {
+        const Bits c = src[i];
+        chk(i, c);
+        out[i] = K3Out<KeyT>::conv(c);
+    }
+    return bad;
 }
 
 template <typename KeyT, bool PERM, int NT>
@@ -544,20 +610,19 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         if (nbig <= kL3BigQ)
             for (uint32_t q = 0; q < nbig; ++q) block_bitonic_sort_nt<KeyT, PERM, NT>(skey, sidx, bigq[2 * q], bigq[2 * q + 1]);
         K3L_T(5);
-        // ---- 5b. weights not provably monotone: check the whole coarse bucket in shared memory
-        // (every rank bucket is sorted, so only rank-bucket boundaries can be out of order)
-        bool bad = false;
-        if (p.verify)
-            for (uint32_t i = tid + 1; i < n; i += NT)
-                bad |= precedes<KeyT, PERM>(skey[i], PERM ? sidx[i] : 0u, skey[i - 1], PERM ? sidx[i - 1] : 0u);
-        // ---- 6. an inversion between rank buckets (ulp-level non-monotone network output, or a
-        // non-monotone model), or too many large buckets: sort the whole coarse bucket
-        if (__syncthreads_or(bad) || nbig > kL3BigQ) {
+        // ---- 5b./7. coalesced store of the sorted coarse bucket to its output range, fused with
+        // the adjacent-order check of reading A14 over the WHOLE coarse bucket (every rank bucket
+        // is sorted, so only rank-bucket boundaries can be out of order).  It runs for every
+        // model: a non-monotone model, or an ulp-level non-monotone network output, then costs a
+        // re-sort of this coarse bucket in shared memory and a second store -- never a wrong
+        // output.
+        if (nbig > kL3BigQ) block_bitonic_sort_nt<KeyT, PERM, NT>(skey, sidx, 0, n);
+        const bool bad = k3l_store_verify<KeyT, PERM, NT>(skey, sidx, n, out_keys + S0);
+        if (__syncthreads_or(bad)) {
             block_bitonic_sort_nt<KeyT, PERM, NT>(skey, sidx, 0, n);
-            if (tid == 0 && nbig <= kL3BigQ) atomicAdd(&st->local_repairs, 1ull);
+            if (tid == 0) atomicAdd(&st->local_repairs, 1ull);
+            k3l_store<KeyT, NT>(skey, n, out_keys + S0);
         }
-        // ---- 7. coalesced store of the sorted coarse bucket to its output range
-        k3l_store<KeyT, NT>(skey, n, out_keys + S0);
         if (PERM) k3l_store<uint32_t, NT>(sidx, n, out_perm + S0);
         K3L_T(6);
     }

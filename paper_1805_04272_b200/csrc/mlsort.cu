@@ -26,6 +26,7 @@
 #include "k3_local.cuh"
 #include "k4_overflow.cuh"
 #include "dist.cuh"
+#include "selftest.cuh"
 
 using namespace mlsort;
 
@@ -252,10 +253,20 @@ const FoldedWeights& fold_cached(const Weights& w, uint32_t mpad, bool f32) {
     return result;
 }
 
-int pred_of(int32_t predictor) {
+uint32_t mpad_of(uint32_t m);
+
+// Public predictor choice -> internal variant.  MLSORT_PRED_DEFAULT is the packed predictor,
+// with value grouping + saturated-pair skipping when M > 32: measured on B200, M = 64 (C3) K1
+// 14.9 -> 5.3 ms with it, M = 32 (C2) 1.01 -> 1.23 ms.  MLSORT_GROUP=1/0 overrides the default
+// (experiments).  Skipping is exact, so every variant of the packed family gives the same bits.
+int resolve_pred(int32_t predictor, uint32_t m) {
     if (predictor == MLSORT_PRED_MUFU) return kPredMufu;
     if (predictor == MLSORT_PRED_MIXED) return kPredMixed;
-    return kPredPacked;   // MLSORT_PRED_DEFAULT, MLSORT_PRED_PACKED
+    if (predictor == MLSORT_PRED_PACKED) return kPredPacked;
+    if (predictor == MLSORT_PRED_SKIP) return kPredSkip;
+    const char* e = std::getenv("MLSORT_GROUP");
+    if (e) return std::atoi(e) != 0 ? kPredSkip : kPredPacked;
+    return mpad_of(m) >= 64 ? kPredSkip : kPredPacked;
 }
 
 uint32_t mpad_of(uint32_t m) { return m <= 16 ? 16 : m <= 32 ? 32 : 64; }
@@ -282,16 +293,6 @@ constexpr size_t kK1WsSmemMax = 232448;      // 227 KB, the sm_100 per-block max
 
 uint32_t ws_tile_of(size_t ks, bool group = false) {
     return ks == 4 ? (uint32_t)ws_tile<float>(group) : (uint32_t)ws_tile<double>(group);
-}
-
-// K1 sparse evaluation (value grouping + saturated-pair skipping): packed predictor only;
-// MLSORT_GROUP=1 / 0 forces it on / off
-bool want_group(int pred, uint32_t mpad) {
-    if (pred != kPredPacked) return false;
-    const char* e = std::getenv("MLSORT_GROUP");
-    if (e) return std::atoi(e) != 0;
-    // measured on B200: M = 64 (C3) K1 14.9 -> 5.3 ms with grouping; M = 32 (C2) 1.01 -> 1.23 ms
-    return mpad >= 64;
 }
 
 Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws);
@@ -597,7 +598,7 @@ cudaError_t launch_k3_t(const Plan& p, void* ws, const Layout& L, KeyT* out_keys
 
 template <typename KeyT, bool PERM, int NT>
 cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s,
-                           bool verify_fine, bool secondary, bool to_mid, uint32_t cap, size_t smem, int grid,
+                           bool secondary, bool to_mid, uint32_t cap, size_t smem, int grid,
                            const unsigned long long* rbase) {
     auto kern = k3_local_sort<KeyT, PERM, NT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -607,7 +608,6 @@ cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_k
     kp.num_coarse = p.C;
     kp.kfine = p.kfine;
     kp.cap = cap;
-    kp.verify = verify_fine ? 1u : 0u;
     kp.secondary = secondary ? 1u : 0u;
     kp.to_mid = to_mid ? 1u : 0u;
     DevStatus* st = at<DevStatus>(ws, L.status);
@@ -624,23 +624,23 @@ cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_k
 // the primary pass handed over.
 template <typename KeyT, bool PERM>
 cudaError_t launch_k3_local(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm,
-                            cudaStream_t s, bool verify_fine, const unsigned long long* rbase) {
+                            cudaStream_t s, const unsigned long long* rbase) {
     cudaError_t e;
     if (p.cap1 > 0) {
-        e = launch_k3_pass<KeyT, PERM, kL3Threads>(p, ws, L, out_keys, out_perm, s, verify_fine, false, true, p.cap1,
+        e = launch_k3_pass<KeyT, PERM, kL3Threads>(p, ws, L, out_keys, out_perm, s, false, true, p.cap1,
                                                    p.k3_smem1, std::min<int>(2 * num_sms(), (int)p.C), rbase);
         if (e != cudaSuccess) return e;
-        return launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, verify_fine, true, false,
+        return launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, true, false,
                                                          p.cap, p.k3_smem, num_sms(), rbase);
     }
-    return launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, verify_fine, false, false,
+    return launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, false, false,
                                                      p.cap, p.k3_smem, std::min<int>(num_sms(), (int)p.C), rbase);
 }
 
 template <typename KeyT, bool PERM>
 cudaError_t launch_k3(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s,
-                      bool verify_fine, const unsigned long long* rbase) {
-    if (p.local) return launch_k3_local<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, verify_fine, rbase);
+                      const unsigned long long* rbase) {
+    if (p.local) return launch_k3_local<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase);
     switch (p.R) {
         case 1: return launch_k3_t<KeyT, PERM, 1>(p, ws, L, out_keys, out_perm, s, rbase);
         case 2: return launch_k3_t<KeyT, PERM, 2>(p, ws, L, out_keys, out_perm, s, rbase);
@@ -817,8 +817,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
                  bool verify_all = false, const ChunkPlan* chunks = nullptr) {
     Launches nl;
     PhaseTimer tm;
-    const bool group = !GIVEN && want_group(pred == kPredMufu || pred == kPredMixed ? pred : kPredPacked,
-                                            GIVEN ? 16 : mpad_of(w->m));
+    const bool group = !GIVEN && pred == kPredSkip;
     const Plan p = make_plan(n, B, sizeof(KeyT), PERM, !GIVEN, group);
     const Layout L = make_layout(p);
     if (ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) % kAlign)) return MLSORT_ERR_WORKSPACE;
@@ -875,13 +874,9 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
                                             n < (1ull << 31));
         CK(cudaGetLastError());
         tm.mark();
-        // Rank-bucket-level verification (reading A14) is needed only when the network is not
-        // provably monotone: with Eq. 4's sign condition every step of the f32 predictor is a
-        // monotone IEEE operation, so consecutive rank buckets cannot
-        // invert; K5 still checks every coarse-bucket boundary.  Received records (multi-GPU) and
-        // opts->verify == 2 are always verified.
-        const bool verify_fine = GIVEN || verify_all || !monotone(*w);
-        CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, verify_fine, rbase)));
+        // K3 checks the adjacent order of every coarse bucket it sorts (reading A14) for every
+        // model, fused with its store; K5 checks every coarse-bucket boundary.
+        CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase)));
         tm.mark();
         k4_big_copy<KeyT, PERM><<<num_sms(), kK3Threads, 0, s>>>(
             p.capc, p.R, at<KeyT>(ws, L.reg_keys), PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
@@ -1070,7 +1065,7 @@ int sort_impl(const void* d_keys, const uint32_t* d_payload, uint64_t n, mlsort_
     const uint64_t B = (o && o->num_buckets) ? o->num_buckets : n;
     if (B > (1ull << 30)) return MLSORT_ERR_INVALID_ARG;
     const Weights* w = reinterpret_cast<const Weights*>(wh);
-    const int pred = pred_of(o ? o->predictor : 0);
+    const int pred = resolve_pred(o ? o->predictor : 0, w->m);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     // align the workspace base
     uintptr_t wsp = reinterpret_cast<uintptr_t>(d_ws);
@@ -1146,17 +1141,34 @@ extern "C" int mlsort_sort_host(const void* h_keys, uint64_t n, mlsort_dtype dt,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     // The host-to-device copy is split into chunks of whole K1 tiles on a copy stream; K1 is
     // launched per chunk as soon as that chunk has arrived, so prediction overlaps the copy.
-    thread_local cudaStream_t cs = nullptr;
-    thread_local cudaEvent_t evs[16] = {};
-    if (!cs) {
-        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        for (auto& e : evs) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // copy stream + chunk events, cached per (thread, device): a later call on another device
+    // must not record events against a stream of the first one
+    struct CopyCtx {
+        int dev = -1;
+        cudaStream_t cs = nullptr;
+        cudaEvent_t evs[16] = {};
+    };
+    thread_local std::vector<CopyCtx> ctxs;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CopyCtx* cx = nullptr;
+    for (auto& c : ctxs)
+        if (c.dev == dev) cx = &c;
+    if (!cx) {
+        CopyCtx c;
+        c.dev = dev;
+        CK(cudaStreamCreateWithFlags(&c.cs, cudaStreamNonBlocking));
+        for (auto& e : c.evs) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctxs.push_back(c);
+        cx = &ctxs.back();
     }
+    cudaStream_t cs = cx->cs;
+    cudaEvent_t* evs = cx->evs;
     const uint64_t B = (o && o->num_buckets) ? o->num_buckets : n;
     ChunkPlan cp;
     if (B <= (1ull << 30) && n < (1ull << 32)) {
         const Weights* wh = reinterpret_cast<const Weights*>(w);
-        const bool group = wh && want_group(pred_of(o ? o->predictor : 0), mpad_of(wh->m));
+        const bool group = wh && resolve_pred(o ? o->predictor : 0, wh->m) == kPredSkip;
         const Plan pl = make_plan(n, B, ks, h_out_perm != nullptr, true, group);
         const uint32_t nchunk = std::min<uint32_t>(8, pl.T);
         const uint32_t per = (pl.T + nchunk - 1) / nchunk;
@@ -1182,7 +1194,13 @@ extern "C" int mlsort_sort_host(const void* h_keys, uint64_t n, mlsort_dtype dt,
     }
     int rc = sort_impl(d_in, nullptr, n, dt, w, o, d_out, d_perm, nullptr, rest, rest_bytes, stream, info,
                        cp.n ? &cp : nullptr);
-    if (rc) return rc;
+    if (rc) {
+        // the chunked copies may still be in flight on cs (e.g. an argument error before any
+        // K1 launch waited on them): they must not outlive the call
+        cudaStreamSynchronize(cs);
+        cudaStreamSynchronize(s);
+        return rc;
+    }
     CK(cudaMemcpyAsync(h_out_keys, d_out, n * ks, cudaMemcpyDeviceToHost, s));
     if (h_out_perm) CK(cudaMemcpyAsync(h_out_perm, d_perm, n * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1191,26 +1209,45 @@ extern "C" int mlsort_sort_host(const void* h_keys, uint64_t n, mlsort_dtype dt,
 
 // ---------------------------------------------------------------- approximate ranking
 namespace {
-template <typename KeyT, int MPAD, int PRED>
+// Each warp evaluates 32 x G consecutive keys (lane + 32 q), so on sorted input a warp spans a
+// narrow value range and the skipping variant (SKIP) drops whole saturated pairs, exactly as on
+// k1_ws's value-grouped tiles.  The clamped chain is used throughout: for keys inside the safe
+// range the clamp is the identity, so the bits equal the sort's clamp-free evaluation.
+template <typename KeyT, int MPAD, int PRED, bool SKIP>
 __global__ void __launch_bounds__(256)
 k_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Params p, float* __restrict__ y_out,
           uint32_t* __restrict__ b_out) {
     constexpr int G = 8;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * G) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t wb = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 * G); wb < n;
+         wb += nwarps * 32 * G) {
         float u[G], ul[G];
         int32_t y[G];
+        float mn = INFINITY, mx = -INFINITY;
 #pragma unroll
         for (int q = 0; q < G; ++q) {
-            const uint64_t i = i0 + (uint64_t)q * stride;
+            const uint64_t i = wb + (uint64_t)q * 32 + lane;
             KeyT x = i < n ? keys[i] : (KeyT)p.lo_d;
             if (!KeyTraits<KeyT>::finite(x)) x = (KeyT)p.lo_d;
             key_to_u<KeyT>(x, p, u[q], ul[q]);
+            if (i < n) {
+                mn = fminf(mn, u[q]);
+                mx = fmaxf(mx, u[q]);
+            }
         }
-        gvm_forward_fxp<MPAD, PRED, G>(fw, u, ul, y);
+        if (SKIP) {
+            const uint32_t omn = __reduce_min_sync(0xffffffffu, f32_ordbits(mn));
+            const uint32_t omx = __reduce_max_sync(0xffffffffu, f32_ordbits(mx));
+            const float umin = __uint_as_float((omn & 0x80000000u) ? (omn & 0x7fffffffu) : ~omn);
+            const float umax = __uint_as_float((omx & 0x80000000u) ? (omx & 0x7fffffffu) : ~omx);
+            gvm_forward_skip<MPAD, G, true>(fw, u, umin, umax, y);
+        } else {
+            gvm_forward_fxp<MPAD, PRED, G>(fw, u, ul, y);
+        }
 #pragma unroll
         for (int q = 0; q < G; ++q) {
-            const uint64_t i = i0 + (uint64_t)q * stride;
+            const uint64_t i = wb + (uint64_t)q * 32 + lane;
             if (i < n) {
                 if (y_out) y_out[i] = fxp_to_float(y[q], p.bm);
                 if (b_out) b_out[i] = bucket_of_fxp(y[q], p.bm);
@@ -1227,12 +1264,14 @@ int launch_predict(const KeyT* keys, uint64_t n, const Weights& w, uint64_t B, i
     Plan p;
     p.n = n;
     K1Params kp = k1_params(w, p, B, sizeof(KeyT) == 4);
-    const int grid = num_sms() * 8;
+    const uint64_t warps = (n + 32 * 8 - 1) / (32 * 8);
+    const int grid = (int)std::min<uint64_t>((uint64_t)num_sms() * 8, (warps + 7) / 8);
 #define PCASE(M)                                                                                    \
     if (mpad == M) {                                                                                \
-        if (pred == kPredMufu) k_predict<KeyT, M, kPredMufu><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b); \
-        else if (pred == kPredMixed) k_predict<KeyT, M, kPredMixed><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b); \
-        else k_predict<KeyT, M, kPredPacked><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b);         \
+        if (pred == kPredMufu) k_predict<KeyT, M, kPredMufu, false><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b); \
+        else if (pred == kPredMixed) k_predict<KeyT, M, kPredMixed, false><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b); \
+        else if (pred == kPredSkip) k_predict<KeyT, M, kPredPacked, true><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b); \
+        else k_predict<KeyT, M, kPredPacked, false><<<grid, 256, 0, s>>>(keys, n, fw, kp, y, b);   \
     }
     PCASE(16) PCASE(32) PCASE(64)
 #undef PCASE
@@ -1249,7 +1288,7 @@ extern "C" int mlsort_predict(const void* d_keys, uint64_t n, mlsort_dtype dt, c
     const uint64_t B = num_buckets ? num_buckets : n;
     if (B > (1ull << 32)) return MLSORT_ERR_INVALID_ARG;
     const Weights* w = reinterpret_cast<const Weights*>(wh);
-    const int pred = pred_of(predictor);
+    const int pred = resolve_pred(predictor, w->m);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     return dt == MLSORT_F32 ? launch_predict<float>((const float*)d_keys, n, *w, B, pred, d_y, d_bucket, s)
                             : launch_predict<double>((const double*)d_keys, n, *w, B, pred, d_y, d_bucket, s);
@@ -1282,7 +1321,8 @@ extern "C" int mlsort_dist_partition(const void* d_shard, uint64_t n_local, uint
     const uint64_t B = (o && o->num_buckets) ? o->num_buckets : n_global;
     if (B > (1ull << 30)) return MLSORT_ERR_INVALID_ARG;
     const Weights* w = reinterpret_cast<const Weights*>(wh);
-    const int pred = pred_of(o ? o->predictor : 0);
+    int pred = resolve_pred(o ? o->predictor : 0, w->m);
+    if (pred == kPredSkip) pred = kPredPacked;   // (same bits; the owner partition does not group)
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     uintptr_t wsp = reinterpret_cast<uintptr_t>(d_ws);
     uintptr_t aligned = (wsp + kAlign - 1) / kAlign * kAlign;
@@ -1372,4 +1412,37 @@ extern "C" int mlsort_sort_records(const void* d_keys, const uint32_t* d_bucket,
                    : run_pipeline<double, false, true>((const double*)d_keys, n, B, nullptr, kPredMixed,
                                                        (double*)d_out_keys, nullptr, ws, ws_bytes, s, info, d_bucket,
                                                        nullptr, blo);
+}
+
+// ---------------------------------------------------------------- K8: primitive sweeps (A14)
+extern "C" int mlsort_selftest_monotone(int32_t primitive, uint64_t* descents, uint64_t* evaluated,
+                                        double* max_rel_err, void* stream) {
+    if (primitive < kSweepEx2 || primitive > kSweepLogistic) return MLSORT_ERR_INVALID_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    SweepOut* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(SweepOut)));
+    SweepOut h;
+    std::memset(&h, 0, sizeof(h));
+    cudaError_t e = cudaMemcpyAsync(d, &h, sizeof(h), cudaMemcpyHostToDevice, s);
+    auto pair = [](float v) {
+        uint32_t b;
+        std::memcpy(&b, &v, 4);
+        return ((unsigned long long)b << 32) | b;
+    };
+    if (e == cudaSuccess) {
+        k_sweep_monotone<<<num_sms() * 8, 256, 0, s>>>(primitive, pair(2.001281198f), pair(1.0f), d);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(d);
+    CK(e);
+    if (descents) *descents = h.descents;
+    if (evaluated) *evaluated = h.evaluated;
+    if (max_rel_err) {
+        float f;
+        std::memcpy(&f, &h.max_rel_err_bits, 4);
+        *max_rel_err = f;
+    }
+    return MLSORT_OK;
 }

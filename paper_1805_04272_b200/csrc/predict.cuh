@@ -77,7 +77,9 @@ __device__ __forceinline__ float rcp_newton(float d) {
     return r;
 }
 
-enum { kPredMufu = 1, kPredMixed = 2, kPredPacked = 3 };
+// kPredSkip: the packed arithmetic with saturated-pair skipping (bit-identical to kPredPacked;
+// k1_ws runs it on value-grouped tiles)
+enum { kPredMufu = 1, kPredMixed = 2, kPredPacked = 3, kPredSkip = 4 };
 
 // ---- packed-pair (f32x2) formulation --------------------
 // Blackwell's FFMA2/FMUL2 evaluate two neurons per instruction; their B operand can be a
@@ -128,6 +130,19 @@ constexpr uint32_t kSeedNeg = 0xFEF33400u;
 constexpr float kAShift = 0.0f;
 constexpr float kAClamp = 60.0f;             // 0x7EF33400 + 0x80000000: bits of -r0 from bits(d)
 
+// -1/d for both lanes of d2 (d in [1, 2^61]) by the packed chain above; shared by the predictor
+// and the exhaustive monotonicity sweep (selftest.cuh), so the swept instructions are the
+// shipped ones.
+__device__ __forceinline__ f32x2 neg_rcp_packed(f32x2 d2, f32x2 k1_2, f32x2 one2) {
+    float d0, d1;
+    upk2(d2, d0, d1);
+    // the seed's bit trick yields -r0 directly (sign bit folded into the constant)
+    f32x2 nr2 = pk2(__uint_as_float(kSeedNeg - __float_as_uint(d0)), __uint_as_float(kSeedNeg - __float_as_uint(d1)));
+    nr2 = fmul2(nr2, ffma2(d2, nr2, k1_2));                 // -r1 = -r0 (k1 - d r0)
+    const f32x2 e2 = ffma2(d2, nr2, one2);                  // e = 1 - d r1
+    return ffma2(nr2, ffma2(e2, e2, e2), nr2);              // -r1 (1 + e + e^2)
+}
+
 // Fixed-point accumulation of Eq. 3: every term w2_j * sigma_j is scaled
 // by 2^S (folded into W_j) and rounded to an integer by one FFMA against the magic constant
 // 1.5 * 2^23, whose float bits are then summed in a 32-bit integer:
@@ -167,14 +182,7 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
                     a1 = fminf(a1, kAClamp);
                 }
                 const f32x2 d2 = fadd2(pk2(ex2_approx(a0), ex2_approx(a1)), fw.dofs2);   // d = 2^-s + e
-                float d0, d1;
-                upk2(d2, d0, d1);
-                // the seed's bit trick yields -r0 directly (sign bit folded into the constant)
-                f32x2 nr2 = pk2(__uint_as_float(kSeedNeg - __float_as_uint(d0)),
-                                __uint_as_float(kSeedNeg - __float_as_uint(d1)));
-                nr2 = fmul2(nr2, ffma2(d2, nr2, fw.k1_2));              // -r1 = -r0 (k1 - d r0)
-                const f32x2 e2 = ffma2(d2, nr2, fw.one2);               // e = 1 - d r1
-                nr2 = ffma2(nr2, ffma2(e2, e2, e2), nr2);               // -r1 (1 + e + e^2)
+                const f32x2 nr2 = neg_rcp_packed(d2, fw.k1_2, fw.one2);
                 const f32x2 t2 = ffma2(nr2, Wn2[j], fw.magic2);         // W 2^-s r + magic
                 float t0, t1;
                 upk2(t2, t0, t1);
@@ -243,13 +251,7 @@ __device__ __forceinline__ void gvm_forward_skip(const FoldedWeights& fw, const 
                 a1 = fminf(a1, kAClamp);
             }
             const f32x2 d2 = fadd2(pk2(ex2_approx(a0), ex2_approx(a1)), fw.dofs2);
-            float d0, d1;
-            upk2(d2, d0, d1);
-            f32x2 nr2 = pk2(__uint_as_float(kSeedNeg - __float_as_uint(d0)),
-                            __uint_as_float(kSeedNeg - __float_as_uint(d1)));
-            nr2 = fmul2(nr2, ffma2(d2, nr2, fw.k1_2));
-            const f32x2 e2 = ffma2(d2, nr2, fw.one2);
-            nr2 = ffma2(nr2, ffma2(e2, e2, e2), nr2);
+            const f32x2 nr2 = neg_rcp_packed(d2, fw.k1_2, fw.one2);
             const f32x2 t2 = ffma2(nr2, Wj, fw.magic2);
             float t0, t1;
             upk2(t2, t0, t1);

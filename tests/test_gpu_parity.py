@@ -67,7 +67,7 @@ def test_sort_sizes(mls, n, dist, dt):
     check_sort(mls, keys, w, p, perm=False)
 
 
-@pytest.mark.parametrize("pred", [1, 2])
+@pytest.mark.parametrize("pred", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("m", [5, 16, 32, 50, 64])
 def test_sort_neuron_counts_and_predictors(mls, m, pred):
     keys = workloads.generate("mixture3", 200003, m, "f32")
@@ -106,7 +106,9 @@ def test_sort_nonmonotone_weights(mls):
     w = mls.Weights.from_dict(pw)
     assert not w.check_monotone()
     info, _ = check_sort(mls, keys, w, w.params(), perm=True)
-    assert info["fallback_used"] == 1 or info["big_buckets"] > 0 or info["repairs"] > 0
+    # (the bit-exact comparison above is the check: a non-monotone model need not invert any
+    # pair of rank buckets that hold keys -- inversions inside one rank bucket are sorted by
+    # the fix-up anyway -- so no repair counter is asserted for this random model)
     # a decreasing model (w1 < 0, Eq. 4 violated for every neuron) inverts the bucket order:
     # the verify pass must catch it and the conventional-sort fallback must repair it
     w = mls.Weights.create(3, [-1, -1, -1], [0.3, 0.3, 0.4], [-0.5, 0, 0.5], [4, 4, 4], -3.0, 3.0)
@@ -171,35 +173,109 @@ def test_sort_host_entry(mls):
 
 # ------------------------------------------------------------------ predict (y, b) parity
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
-@pytest.mark.parametrize("pred", [1, 2])
-def test_predict_parity(mls, name, pred):
-    cfg = workloads.CONFIGS[name]
-    n = 1 << 18
-    keys = workloads.generate_config(cfg, n=n)
-    w, p = _fit(mls, keys, cfg.m, n0=min(cfg.n0, n // 4), seed=cfg.train_seed)
-    B = cfg.buckets
+def _cfg_weights(mls, name):
+    """The config's stored weights (workloads/weights/<name>.json, data shared by both sides):
+    the product handle and the oracle's plain dict."""
+    return mls.Weights.load(workloads.weights_path(name)), workloads.load_weights_dict(name)
+
+
+def _db_hist(db):
+    v, c = np.unique(db, return_counts=True)
+    return {int(a): int(b) for a, b in zip(v, c)}
+
+
+def _check_predict(mls, name, keys, w, p, pred, B):
     y, b = mls.predict(_t(keys), w, num_buckets=B, predictor=pred)
     y = y.cpu().numpy().astype(np.float64)
     b = b.cpu().numpy().astype(np.int64)
     y_ref = oracle.predict(p, keys)
     b_ref = oracle.bucket(y_ref, B).astype(np.int64)
-    dy = np.max(np.abs(y - y_ref))
-    assert dy <= 1e-5, dy
-    db = np.max(np.abs(b - b_ref))
-    bound = 1 if name == "C1" else 1 + math.ceil(B * dy)
-    assert db <= bound, (db, bound, dy)
+    dy = float(np.max(np.abs(y - y_ref)))
+    db = b - b_ref
+    bound = 1 if name == "C1" else 1 + math.ceil(B * dy)           # reading A17
+    print(f"{name} pred={pred} n={len(keys)} max|dy|={dy:.3e} |db|<={bound} db-histogram={_db_hist(db)}")
+    assert dy <= 1e-5, dy                                            # BJ:5
+    assert int(np.max(np.abs(db))) <= bound, (int(np.max(np.abs(db))), bound, dy)
+    return y, b
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+@pytest.mark.parametrize("pred", [0, 1, 2, 3, 4])
+def test_predict_parity(mls, name, pred):
+    """|dy| <= 1e-5 and the A17 bucket bound for every predictor variant (0 = the sort's
+    default: PACKED for M <= 32, SKIP for M = 64) on 2^18 keys of each config."""
+    cfg = workloads.CONFIGS[name]
+    keys = workloads.generate_config(cfg, n=1 << 18)
+    w, p = _cfg_weights(mls, name)
+    _check_predict(mls, name, keys, w, p, pred, cfg.buckets)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_predict_parity_every_key(mls, name):
+    """Reading A16: every key of C1 and C2 with the shipped (default) predictor."""
+    cfg = workloads.CONFIGS[name]
+    keys = workloads.generate_config(cfg)
+    w, p = _cfg_weights(mls, name)
+    _check_predict(mls, name, keys, w, p, 0, cfg.buckets)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_predict_parity_subset_2e24(mls, name):
+    """Reading A16: a 2^24-key seeded subset of C3-C5 (drawn across the whole config) with the
+    shipped (default) predictor."""
+    cfg = workloads.CONFIGS[name]
+    start = (cfg.n // 3) & ~3
+    keys = workloads.generate_config(cfg, n=1 << 24, start=start)
+    w, p = _cfg_weights(mls, name)
+    _check_predict(mls, name, keys, w, p, 0, cfg.buckets)
+
+
+@pytest.mark.parametrize("m,dist,dt", [(16, "uniform01", "f32"), (32, "normal", "f32"), (64, "mixture3", "f32"),
+                                       (64, "lognormal", "f64"), (50, "normal", "f64")])
+@pytest.mark.parametrize("order", ["random", "sorted"])
+def test_skip_bit_identical(mls, m, dist, dt, order):
+    """Saturated-pair skipping (MLSORT_PRED_SKIP, the sort's M=64 path) is exact: y and b are
+    bit-identical to the full packed evaluation; sorted input makes every warp's key range
+    narrow, so most pairs are skipped."""
+    keys = workloads.generate(dist, 1 << 20, 17, dt)
+    if order == "sorted":
+        keys = np.sort(keys)
+    w, _ = _fit(mls, keys, m, n0=1 << 14, seed=5)
+    y3, b3 = mls.predict(_t(keys), w, predictor=3)
+    y4, b4 = mls.predict(_t(keys), w, predictor=4)
+    assert bool((y3.view(torch_int32()) == y4.view(torch_int32())).all())
+    assert bool((b3 == b4).all())
+
+
+def torch_int32():
+    import torch
+    return torch.int32
+
+
+# ------------------------------------------------------------------ the shipped sort paths
+
+@pytest.mark.parametrize("dist,dt,m,pred", [("mixture3", "f32", 64, 0),     # C4 shape: grouped f32 + perm
+                                            ("lognormal", "f64", 64, 0),    # C3 shape: grouped f64 + perm
+                                            ("normal", "f32", 32, 4),       # grouped forced at M = 32
+                                            ("mixture3", "f32", 64, 3)])    # ungrouped forced at M = 64
+def test_sort_grouped_paths_exact(mls, dist, dt, m, pred):
+    """Bit-exact sorts (keys and permutation) against the oracle's algorithm on 2^22 keys for
+    every K1 variant the library ships (value-grouped k1_ws with skipping, f32/f64, perm)."""
+    keys = workloads.generate(dist, 1 << 22, 23, dt)
+    w, p = _fit(mls, keys, m, n0=1 << 16, seed=7)
+    info, _ = check_sort(mls, keys, w, p, perm=True, predictor=pred)
+    assert info["fallback_used"] == 0, info
+    check_sort(mls, keys, w, p, perm=False, predictor=pred)
 
 
 # ------------------------------------------------------------------ full-size configs
 
 @pytest.mark.parametrize("name", ["C1", "C2"])
 def test_full_config_exact(mls, name):
+    """C1, C2 at full size against the oracle's step-by-step algorithm."""
     cfg = workloads.CONFIGS[name]
     keys = workloads.generate_config(cfg)
-    sample = workloads.draw_sample(keys, cfg.n0, cfg.sample_seed)
-    w = mls.Weights.fit(sample, m=cfg.m, seed=cfg.train_seed)
-    p = w.params()
+    w, p = _cfg_weights(mls, name)
     ref = oracle.ml_sort(keys, p, B=cfg.buckets)
     k, pm, info = mls.sort(_t(keys), w, perm=cfg.perm, num_buckets=cfg.buckets)
     np.testing.assert_array_equal(_bits(k.cpu().numpy()), _bits(ref["keys"]))
@@ -208,37 +284,29 @@ def test_full_config_exact(mls, name):
     assert info["fallback_used"] == 0
 
 
-@pytest.mark.parametrize("name", ["C3", "C5"])
-def test_full_config_sampled(mls, name):
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_full_config_exact_large(mls, name):
+    """C3 (2^28 f64), C4 (2^30 f32 + perm, one GPU) and C5 (2^29 + perm) at full size, element
+    by element against the plain definition of the result (oracle.sorted_reference: stable
+    sort of (key, index) under totalOrder; BJ:5 "bit-exact with the oracle on all five
+    configs")."""
     import torch
     cfg = workloads.CONFIGS[name]
     keys = workloads.generate_config(cfg)
-    sample = workloads.draw_sample(keys, cfg.n0, cfg.sample_seed)
-    w = mls.Weights.fit(sample, m=cfg.m, seed=cfg.train_seed)
-    p = w.params()
-    kt = _t(keys)
-    k, pm, info = mls.sort(kt, w, perm=cfg.perm, num_buckets=cfg.buckets)
-    # properties at full size: non-decreasing (key, index) and a true permutation
-    assert bool((k[1:] >= k[:-1]).all())                 # no zeros of both signs in C3/C5
-    if cfg.perm:
-        pi = pm.to(torch.int64)
-        seen = torch.zeros(cfg.n, dtype=torch.int32, device="cuda")
-        seen.index_add_(0, pi, torch.ones_like(pm))
-        assert bool((seen == 1).all())
-        assert bool((kt[pi] == k).all())
-        tie = k[1:] == k[:-1]
-        assert bool((pi[1:][tie] > pi[:-1][tie]).all())
-    # sampled positions against the oracle's plain definition
-    pos = np.random.default_rng(1).integers(0, cfg.n, 4)
-    ek, ei = oracle.select_sorted(keys, pos)
-    got = k[torch.from_numpy(pos).cuda()].cpu().numpy()
-    np.testing.assert_array_equal(_bits(got), _bits(ek))
-    if cfg.perm:
-        np.testing.assert_array_equal(pm[torch.from_numpy(pos).cuda()].cpu().numpy(), ei)
-    # sampled y / bucket parity at full size
-    sub = keys[pos]
-    y, b = mls.predict(_t(sub), w, num_buckets=cfg.buckets)
-    assert np.max(np.abs(y.cpu().numpy() - oracle.predict(p, sub))) <= 1e-5
+    w, _ = _cfg_weights(mls, name)
+    k, pm, info = mls.sort(_t(keys), w, perm=cfg.perm, num_buckets=cfg.buckets)
+    print(name, {x: info[x] for x in ("num_coarse", "max_coarse", "big_buckets", "repairs", "fallback_used")})
+    got_k = k.cpu().numpy()
+    got_p = pm.cpu().numpy().view(np.uint32) if cfg.perm else None
+    del k, pm
+    torch.cuda.empty_cache()
+    ref_k, ref_p = oracle.sorted_reference(keys, want_perm=cfg.perm)
+    del keys
+    step = 1 << 26                                           # compare in chunks
+    for s0 in range(0, cfg.n, step):
+        np.testing.assert_array_equal(_bits(got_k[s0:s0 + step]), _bits(ref_k[s0:s0 + step]))
+        if cfg.perm:
+            np.testing.assert_array_equal(got_p[s0:s0 + step], ref_p[s0:s0 + step])
 
 
 # ------------------------------------------------------------------ K8: exhaustive monotonicity
@@ -263,21 +331,36 @@ def _all_finite_f32_ascending(chunk_bits):
         start += n
 
 
+@pytest.mark.parametrize("prim", [0, 1, 2, 3])
+def test_k8_primitive_sweeps(mls, prim):
+    """Reading A14 / K8 part 2: every approximate primitive of the device predictor is
+    monotone over its WHOLE domain -- ex2.approx.ftz.f32 on all 2^32 - 2^24 non-NaN f32,
+    the packed reciprocal chain on every f32 d in [1, 2^61] (max |r d - 1| reported),
+    rcp.approx.ftz.f32 on every positive f32, and the packed logistic term on every a."""
+    r = mls.selftest_monotone(prim)
+    print("sweep", prim, r)
+    expect = {0: (1 << 32) - 2 * ((1 << 23) - 1), 1: 0x5E000000 - 0x3F800000 + 1, 2: 0x7F7FFFFF,
+              3: (1 << 32) - 2 * ((1 << 23) - 1)}[prim]
+    assert r["evaluated"] == expect
+    assert r["descents"] == 0, r
+    if prim == 1:
+        assert r["max_rel_err"] < 2.4e-7, r        # a few ulp: far inside the 1e-5 budget
+
+
 @pytest.mark.slow
-@pytest.mark.parametrize("pred", [0, 1, 2])
-def test_k8_predictor_monotone_over_all_f32(mls, pred):
+@pytest.mark.parametrize("name,pred", [("C1", 0), ("C2", 0), ("C2", 1), ("C2", 2), ("C4", 0)])
+def test_k8_predictor_monotone_over_all_f32(mls, name, pred):
     """SURVEY §8(c) pin "predictor y (GPU side): exhaustive monotonicity of K1 over all finite
-    f32 u": with sign-feasible (Eq. 4) weights the device network output and bucket are
-    non-decreasing over every finite float32 key in ascending order (~4.28e9 keys).  f64 keys
-    reach the network only through fl32(x - lo), so this covers them too."""
-    import torch
-    cfg = workloads.CONFIGS["C2"]
-    keys = workloads.generate_config(cfg, n=1 << 18)
-    w, _ = _fit(mls, keys, cfg.m, n0=1 << 14, seed=cfg.train_seed)
+    f32 u": with a config's sign-feasible (Eq. 4) weights the device network output and bucket
+    are non-decreasing over every finite float32 key in ascending order (~4.28e9 keys).
+    pred 0 for C4 (M = 64) is the skipping predictor the sort runs (f32 configs: the swept
+    keys are exactly the inputs the sort can receive)."""
+    cfg = workloads.CONFIGS[name]
+    w, _ = _cfg_weights(mls, name)
     assert w.check_monotone()
     last_y, last_b, total = None, None, 0
     for x in _all_finite_f32_ascending(1 << 28):
-        y, b = mls.predict(x, w, num_buckets=1 << 26, predictor=pred)
+        y, b = mls.predict(x, w, num_buckets=cfg.buckets, predictor=pred)
         assert bool((y[1:] >= y[:-1]).all()), "network output decreases somewhere"
         assert bool((b[1:] >= b[:-1]).all()), "bucket decreases somewhere"
         if last_y is not None:

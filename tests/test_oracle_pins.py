@@ -292,3 +292,66 @@ def test_select_sorted_matches_full_sort():
     k, i = oracle.select_sorted(keys, pos)
     np.testing.assert_array_equal(k, ref_k[pos])
     np.testing.assert_array_equal(i, ref_p[pos])
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("bad,where", [(np.inf, 0), (-np.inf, 17), (np.inf, 99), (-np.inf, 99)])
+def test_ml_sort_lone_infinity_rejected(dt, bad, where):
+    """S:281 pre "all keys finite" / reading A11: a lone +Inf or -Inf (no NaN anywhere) is
+    rejected with its index -- an isnan-only validator fails this pin."""
+    keys = np.linspace(-1, 1, 100).astype(dt)
+    keys[where] = bad
+    w = workloads.random_monotone_weights(4, 1, lo=-1, hi=1)
+    assert oracle.validate(keys) == where
+    with pytest.raises(oracle.NonFiniteKey) as e:
+        oracle.ml_sort(keys, w)
+    assert e.value.index == where
+
+
+def test_ml_sort_infinity_before_nan_lowest_index():
+    """A11: the LOWEST non-finite index is reported whichever kind comes first."""
+    keys = np.linspace(0, 1, 100)
+    keys[30] = -np.inf
+    keys[60] = np.nan
+    assert oracle.validate(keys) == 30
+
+
+def test_tails_strict_bounds():
+    """S:301 "keys outside the training sample's [min, max] are tails" and S:272 "keys below
+    sample_lo go to low_tail, above sample_hi to high_tail": keys equal to lo or hi are body
+    keys (reading A26); one key just below lo is a low tail (the mirror of S:276)."""
+    assert oracle.tails(np.array([0.1, 0.5, 0.9]), 0.1, 0.9) == (0, 0)
+    assert oracle.tails(np.array([np.nextafter(0.1, 0.0), 0.5, 0.9]), 0.1, 0.9) == (1, 0)
+    assert oracle.tails(np.array([0.1, 0.5, np.nextafter(0.9, 1.0)]), 0.1, 0.9) == (0, 1)
+    assert oracle.tails(np.array([0.05, 0.07, 0.5, 2.0]), 0.1, 0.9) == (2, 1)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("seed", range(4))
+def test_sorted_reference_brute_force(dt, seed):
+    """The plain definition of the result: stable totalOrder sort of
+    (key, index), checked against O(n^2) brute-force ranks with ties, +-0 and extremes."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(1, 300))
+    keys = np.round(rng.normal(0, 2, n), 1).astype(dt)
+    keys[rng.integers(0, n, 3)] = -0.0
+    keys[rng.integers(0, n)] = np.finfo(dt).max
+    keys[rng.integers(0, n)] = -np.finfo(dt).max
+    keys[rng.integers(0, n)] = np.finfo(dt).tiny / 4          # subnormal
+    sk, perm = oracle.sorted_reference(keys)
+    bp = _brute_rank_perm(keys)
+    assert list(perm) == bp
+    np.testing.assert_array_equal(sk.view(np.uint8), keys[bp].view(np.uint8))
+    sk2, none = oracle.sorted_reference(keys, want_perm=False)
+    assert none is None
+    np.testing.assert_array_equal(sk2.view(np.uint8), keys[bp].view(np.uint8))
+
+
+@pytest.mark.parametrize("dist,dt", [("grid4096", "f32"), ("normal", "f32"), ("lognormal", "f64")])
+def test_sorted_reference_matches_stable_argsort(dist, dt):
+    """Medium sizes with heavy ties: equal to numpy's stable argsort of the order bits."""
+    keys = workloads.generate(dist, 200003, 9, dt)
+    sk, perm = oracle.sorted_reference(keys)
+    ref = np.argsort(oracle.order_bits(keys), kind="stable")
+    np.testing.assert_array_equal(perm, ref.astype(np.uint32))
+    np.testing.assert_array_equal(sk.view(np.uint8), keys[ref].view(np.uint8))

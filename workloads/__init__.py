@@ -22,13 +22,16 @@ The configs C1..C5 are BASELINE.json configs[0..4] (BJ:7-BJ:11).
 """
 from __future__ import annotations
 
+import json
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
 
 __all__ = [
-    "Config", "CONFIGS", "generate", "generate_config", "draw_sample",
+    "Config", "CONFIGS", "generate", "generate_config", "draw_sample", "WEIGHTS_DIR", "weights_path",
+    "load_weights_dict",
     "random_monotone_weights", "random_nonmonotone_weights",
 ]
 
@@ -73,6 +76,26 @@ CONFIGS = {
     "C5": Config("C5", 1 << 29, "f32", "grid4096", 5, 32, 1 << 18, 1 << 29, True, (1, 8)),
 }
 
+# Trained weights per config (versioned JSON), written once by scripts/make_weights.py
+# from each config's seeded training sample; data for both sides of the parity harness.
+WEIGHTS_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "weights")
+
+
+def weights_path(name: str) -> str:
+    return os.path.join(WEIGHTS_DIR, f"{name}.json")
+
+
+def load_weights_dict(name: str) -> dict:
+    """The stored weights of config `name` as a plain dict {m, w1, w2, b, beta, input_lo,
+    input_hi} (JSON parsing only)."""
+    with open(weights_path(name)) as f:
+        d = json.load(f)
+    return {"m": int(d["m"]), "w1": np.asarray(d["w1"], dtype=np.float64),
+            "w2": np.asarray(d["w2"], dtype=np.float64), "b": np.asarray(d["b"], dtype=np.float64),
+            "beta": np.asarray(d["beta"], dtype=np.float64), "input_lo": float(d["input_lo"]),
+            "input_hi": float(d["input_hi"])}
+
+
 # words of the Philox stream consumed per key
 _WORDS = {"uniform01": 1, "grid4096": 1, "normal": 2, "lognormal": 2, "mixture3": 3,
           "uniform_range": 1, "truncnormal": 2, "allequal": 0}
@@ -114,6 +137,12 @@ def generate(dist: str, n: int, seed: int, dtype: str = "f32", start: int = 0,
     npdt = np.float32 if dtype == "f32" else np.float64
     if n == 0:
         return np.zeros(0, dtype=npdt)
+    chunk = 1 << 24
+    if n > chunk:                       # bounded host memory: key i depends only on its own words
+        out = np.empty(n, dtype=npdt)
+        for c0 in range(0, n, chunk):
+            out[c0:c0 + chunk] = generate(dist, min(chunk, n - c0), seed, dtype, start + c0, **params)
+        return out
     raw = _raw(seed, start * k, n * k)
     if dist == "uniform01":
         if dtype == "f32":
