@@ -46,7 +46,8 @@ enum mlsort_status_code {
     MLSORT_ERR_WORKSPACE = 7,        /* workspace too small or misaligned                */
     MLSORT_ERR_CAPACITY = 8,         /* distributed output larger than out_capacity      */
     MLSORT_ERR_TRAIN = 9,            /* degenerate training sample (all keys equal)      */
-    MLSORT_ERR_INTERNAL = 10         /* internal invariant violated (a bug)              */
+    MLSORT_ERR_INTERNAL = 10,        /* internal invariant violated (a bug)              */
+    MLSORT_ERR_NCCL = 11             /* NCCL missing (libnccl.so.2) or an NCCL call failed */
 };
 
 typedef enum { MLSORT_F32 = 0, MLSORT_F64 = 1 } mlsort_dtype;
@@ -223,10 +224,15 @@ int mlsort_selftest_monotone(int32_t primitive, uint64_t* descents, uint64_t* ev
  * One process per GPU.  Rank g holds the contiguous input slice
  * starting at global index `global_offset`; every rank predicts the global bucket
  * b = round(y*B) of its keys and the owner rank floor(b*G/B), so rank g owns the rank
- * range [gB/G, (g+1)B/G) (BJ:5).  The caller exchanges the records with one all-to-all
- * (torch.distributed / NCCL) and then sorts what it received with
- * mlsort_sort_records.  Concatenating the ranks' outputs in rank order gives the
- * global sorted array, identical to the 1-GPU result. */
+ * range [gB/G, (g+1)B/G) (BJ:5).  mlsort_sort_dist (below) runs the whole exchange with a
+ * library-owned NCCL communicator; the two building blocks are exported for callers that
+ * move the records themselves.  Concatenating the ranks' outputs in rank order gives the
+ * global sorted array, identical to the 1-GPU result.
+ * A model that fails Eq. 4 (mlsort_weights_check_monotone == 0) does not order the
+ * buckets; mlsort_dist_partition then routes keys by key value instead (owner =
+ * clamp(floor((x - input_lo) G / (input_hi - input_lo)), 0, G-1), monotone in x),
+ * reports info->fallback_used = 1, and the receivers must sort with the bucket range
+ * [0, B) (reading A14). */
 
 int mlsort_dist_partition_workspace_size(uint64_t n_local, mlsort_dtype dtype, uint32_t nranks,
                                          uint64_t* bytes);
@@ -236,6 +242,7 @@ int mlsort_dist_partition_workspace_size(uint64_t n_local, mlsort_dtype dtype, u
  *   d_rec_keys [n_local] keys (dtype), d_rec_bucket [n_local] global bucket b (uint32),
  *   d_rec_index [n_local] global input index (uint32; global_offset + local index).
  *   h_send_counts [nranks] (host) number of records for each destination.
+ * info->fallback_used = 1: routed by key value (non-monotone model, see above).
  * Synchronises `stream`.  Errors as mlsort_sort (non-finite keys, bad args). */
 int mlsort_dist_partition(const void* d_shard, uint64_t n_local, uint64_t global_offset,
                           uint64_t n_global, mlsort_dtype dtype, const mlsort_weights* w,
@@ -253,6 +260,60 @@ int mlsort_sort_records(const void* d_keys, const uint32_t* d_bucket, const uint
                         uint64_t n, mlsort_dtype dtype, uint64_t bucket_lo, uint64_t bucket_hi,
                         void* d_out_keys, uint32_t* d_out_index, void* d_ws, uint64_t ws_bytes,
                         void* stream, mlsort_info* info);
+
+/* ------------------------------------------------------------------ multi-GPU sort (NCCL)
+ * SURVEY.md §8(b)/(e); PAPER.md l.94 ("the prediction of each number is independent ...
+ * requires very little networking workload"), l.134 ("both N and M can be separated").
+ * One process per GPU; the library owns an NCCL communicator (libnccl.so.2 is loaded at
+ * mlsort_comm_init; MLSORT_NCCL_LIB overrides its path).  Every call below is collective
+ * over the communicator's ranks, in the same order, with consistent arguments; argument
+ * errors are detected locally (not collectively) and are caller bugs. */
+typedef struct mlsort_comm mlsort_comm;
+
+/* Fill out_id (128 bytes, NCCL_UNIQUE_ID_BYTES) with a fresh NCCL unique id: called on one
+ * rank, which then broadcasts the bytes to the others (e.g. torch.distributed).
+ * Errors: MLSORT_ERR_INVALID_ARG, MLSORT_ERR_NCCL. */
+int mlsort_comm_unique_id(void* out_id);
+
+/* Create this rank's communicator on CUDA device `device` (ncclCommInitRank; collective).
+ * nranks in [1, 64].  The caller owns *out and frees it with mlsort_comm_destroy.
+ * Errors: MLSORT_ERR_INVALID_ARG, MLSORT_ERR_CUDA, MLSORT_ERR_NCCL. */
+int mlsort_comm_init(int nranks, int rank, const void* unique_id, int device, mlsort_comm** out);
+
+/* Destroy a communicator (NULL is a no-op).  Errors: MLSORT_ERR_NCCL. */
+int mlsort_comm_destroy(mlsort_comm* comm);
+
+/* Device workspace of mlsort_sort_dist for a rank holding n_local keys that may receive up
+ * to out_capacity records (its output capacity). */
+int mlsort_sort_dist_workspace_size(uint32_t nranks, uint64_t n_local, uint64_t n_global, mlsort_dtype dtype,
+                                    const mlsort_opts* opts, int want_perm, uint64_t out_capacity,
+                                    uint64_t* bytes);
+
+/* Distributed sort of the global array whose keys [global_offset, global_offset + n_local)
+ * are on this rank (device pointer d_shard; n_global < 2^32, B = opts->num_buckets or
+ * n_global).  Steps: predict + owner partition (global buckets, owner floor(b G / B)); an
+ * NCCL all-gather of the send counts; one grouped NCCL send/recv all-to-all-v of the
+ * records (key, bucket, global index), received in source-rank order; the local sort of the
+ * received records (no re-prediction); an NCCL all-gather of every rank's first/last
+ * (key, index) that verifies the order across ranks and gives the global offset.
+ * Outputs: d_out_keys[*out_count] = this rank's sorted run, d_out_perm (nullable; GLOBAL
+ * input indices, stable), *out_global_offset = position of the run in the global sorted
+ * array (sum of the lower ranks' counts).  The concatenation over ranks equals mlsort_sort
+ * of the whole array on one GPU, bit for bit.  Caller owns every buffer; d_ws from
+ * mlsort_sort_dist_workspace_size.  With opts->timing, info->phase_ms = {partition, count
+ * exchange, all-to-all, local sort, boundary exchange, total}.
+ * Errors (collective: every rank returns the same code):
+ *   MLSORT_ERR_NONFINITE_KEY  info->bad_index = lowest GLOBAL index of a NaN/+-Inf key;
+ *   MLSORT_ERR_CAPACITY       some rank would receive more than its out_capacity;
+ *                             *out_count = this rank's required capacity;
+ *   MLSORT_ERR_INTERNAL       the cross-rank order check failed (not reachable with either
+ *                             ownership rule, which are monotone in the key);
+ *   MLSORT_ERR_NCCL / MLSORT_ERR_CUDA / MLSORT_ERR_WORKSPACE. */
+int mlsort_sort_dist(mlsort_comm* comm, const void* d_shard, uint64_t n_local, uint64_t global_offset,
+                     uint64_t n_global, mlsort_dtype dtype, const mlsort_weights* w, const mlsort_opts* opts,
+                     void* d_out_keys, uint32_t* d_out_perm, uint64_t out_capacity, uint64_t* out_count,
+                     uint64_t* out_global_offset, void* d_ws, uint64_t ws_bytes, void* stream,
+                     mlsort_info* info);
 
 #ifdef __cplusplus
 }

@@ -27,7 +27,8 @@ PRED_DEFAULT, PRED_MUFU, PRED_MIXED, PRED_PACKED, PRED_SKIP = 0, 1, 2, 3, 4
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "I/O error", 3: "weights JSON parse error",
           4: "invalid weights", 5: "non-finite key", 6: "CUDA error", 7: "workspace",
-          8: "capacity", 9: "degenerate training sample", 10: "internal error"}
+          8: "capacity", 9: "degenerate training sample", 10: "internal error", 11: "NCCL"}
+ERR_CAPACITY = 8
 
 
 class MLSortError(RuntimeError):
@@ -102,6 +103,12 @@ def lib():
         L.mlsort_sort_records_workspace_size.argtypes = [u64, i32, u64, u64, C.POINTER(u64)]
         L.mlsort_sort_records.argtypes = [P, P, P, u64, i32, u64, u64, P, P, P, u64, P, C.POINTER(Info)]
         L.mlsort_selftest_monotone.argtypes = [i32, C.POINTER(u64), C.POINTER(u64), C.POINTER(d), P]
+        L.mlsort_comm_unique_id.argtypes = [P]
+        L.mlsort_comm_init.argtypes = [C.c_int, C.c_int, P, C.c_int, C.POINTER(P)]
+        L.mlsort_comm_destroy.argtypes = [P]
+        L.mlsort_sort_dist_workspace_size.argtypes = [u32, u64, u64, i32, C.POINTER(_Opts), i32, u64, C.POINTER(u64)]
+        L.mlsort_sort_dist.argtypes = [P, P, u64, u64, u64, i32, P, C.POINTER(_Opts), P, P, u64, C.POINTER(u64),
+                                       C.POINTER(u64), P, u64, P, C.POINTER(Info)]
         _lib = L
     return _lib
 
@@ -401,6 +408,89 @@ def sort_records(keys, bucket, index, bucket_lo: int, bucket_hi: int, stream=Non
                                    C.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream), C.byref(info))
     _check(rc, "mlsort_sort_records", info)
     return out_k, out_i, info.as_dict()
+
+
+class Comm:
+    """Library-owned NCCL communicator over a torch.distributed group (mlsort_comm_init): rank 0
+    creates the NCCL unique id, torch.distributed broadcasts it, every rank joins on its device."""
+
+    def __init__(self, group=None, device=None):
+        torch = _torch()
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            _check(lib().mlsort_comm_unique_id(uid), "mlsort_comm_unique_id")
+        obj = [bytes(uid)]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=group)
+        buf = C.create_string_buffer(obj[0], 128)
+        h = C.c_void_p()
+        _check(lib().mlsort_comm_init(self.world, self.rank, buf, self.device.index or 0, C.byref(h)),
+               "mlsort_comm_init")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().mlsort_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def workspace_size(self, n_local: int, n_global: int, dtype_code: int, perm: bool, capacity: int,
+                       num_buckets: int = 0) -> int:
+        b = C.c_uint64()
+        o = _opts(num_buckets, 0)
+        _check(lib().mlsort_sort_dist_workspace_size(self.world, n_local, n_global, dtype_code, C.byref(o),
+                                                      1 if perm else 0, capacity, C.byref(b)),
+               "mlsort_sort_dist_workspace_size")
+        return b.value
+
+    def sort(self, shard, weights: "Weights", global_offset: int, n_global: int, perm: bool = False,
+             num_buckets: int = 0, capacity: int | None = None, predictor: int = PRED_DEFAULT,
+             timing: bool = False, out_keys=None, out_perm=None, workspace=None, stream=None):
+        """Collective distributed sort (mlsort_sort_dist).  Returns (keys, perm or None,
+        global_offset, info); keys is this rank's sorted run.  On MLSORT_ERR_CAPACITY (collective)
+        the buffers are re-allocated to the reported sizes and the call is repeated."""
+        torch = _torch()
+        n = shard.numel()
+        dt = _dtype_code(shard)
+        if capacity is None:
+            capacity = max(1024, 2 * (n_global + self.world - 1) // self.world)
+        for _ in range(2):
+            if out_keys is None or out_keys.numel() < capacity:
+                out_keys = torch.empty(capacity, dtype=shard.dtype, device=shard.device)
+            if perm and (out_perm is None or out_perm.numel() < capacity):
+                out_perm = torch.empty(capacity, dtype=torch.int32, device=shard.device)
+            wsb = self.workspace_size(n, n_global, dt, perm, capacity, num_buckets)
+            if workspace is None or workspace.numel() < wsb:
+                workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=shard.device)
+            o = _opts(num_buckets, predictor, timing)
+            info = Info()
+            cnt, goff = C.c_uint64(), C.c_uint64()
+            rc = lib().mlsort_sort_dist(self._h, C.c_void_p(shard.data_ptr()) if n else None, n, global_offset,
+                                        n_global, dt, weights.handle, C.byref(o), C.c_void_p(out_keys.data_ptr()),
+                                        C.c_void_p(out_perm.data_ptr()) if perm else None, capacity, C.byref(cnt),
+                                        C.byref(goff), C.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                        _stream_ptr(stream), C.byref(info))
+            if rc == ERR_CAPACITY:                     # every rank got it: grow to the largest need
+                import torch.distributed as dist
+                t = torch.tensor([cnt.value], dtype=torch.int64, device=shard.device)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                capacity = int(t.item())
+                continue
+            _check(rc, "mlsort_sort_dist", info)
+            k = out_keys[:cnt.value]
+            pm = out_perm[:cnt.value] if perm else None
+            self.last = (out_keys, out_perm, workspace)
+            return k, pm, goff.value, info
+        raise MLSortError(ERR_CAPACITY, "mlsort_sort_dist")
 
 
 SWEEP_EX2, SWEEP_RCP_CHAIN, SWEEP_RCP_MUFU, SWEEP_LOGISTIC = 0, 1, 2, 3

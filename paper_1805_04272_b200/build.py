@@ -12,7 +12,10 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libmlsort.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["mlsort.cu", "host_weights.cpp", "host_train.cpp"]
+SOURCES = ["mlsort.cu", "host_weights.cpp", "host_train.cpp", "comm.cpp"]
+# NCCL headers (torch-bundled); the library is dlopen-ed at run time (csrc/comm.cpp)
+NCCL_INC = os.environ.get("MLSORT_NCCL_INC", os.path.join(os.path.dirname(sys.executable), "..", "lib",
+                          "python%d.%d" % sys.version_info[:2], "site-packages", "nvidia", "nccl", "include"))
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -46,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
         else:
-            cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-I", INCLUDE, "-I", "/usr/local/cuda/include",
+            cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-I", INCLUDE, "-I", "/usr/local/cuda/include", "-I", NCCL_INC,
                    "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
@@ -58,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and out:
             sys.stderr.write(out.decode(errors="replace"))
     tmp = LIB + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, *GENCODE, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs])
+    subprocess.check_call([NVCC, *GENCODE, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -18,9 +18,28 @@ __device__ __forceinline__ uint32_t owner_of(uint32_t b, uint64_t B, uint32_t G)
     return (uint32_t)(((uint64_t)b * G) / B);
 }
 
+// Ownership rule of one exchange.  Monotone model (Eq. 4): owner = floor(b*G/B), the rank
+// range of BJ:5.  A model that fails Eq. 4 does not order the buckets, so its keys are routed
+// by key value instead -- owner = clamp(floor((x - lo) G / (hi - lo)), 0, G-1), monotone in x
+// by construction -- and each receiver sorts whatever buckets it gets (reading A14).
+struct OwnerRule {
+    uint64_t B;
+    uint32_t G;
+    uint32_t keyspace;      // 1: route by key value
+    double lo, scale;       // keyspace: owner = floor((x - lo) * scale), scale = G / (hi - lo)
+};
+
+template <typename KeyT>
+__device__ __forceinline__ uint32_t owner_rule(const OwnerRule& r, KeyT x, uint32_t b) {
+    if (!r.keyspace) return owner_of(b, r.B, r.G);
+    const double t = ((double)x - r.lo) * r.scale;
+    if (!(t > 0.0)) return 0u;
+    return t >= (double)(r.G - 1) ? r.G - 1 : (uint32_t)t;
+}
+
 template <typename KeyT, int MPAD, int PRED>
 __global__ void __launch_bounds__(kRadixThreads)
-k_dist_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Params p, uint64_t B, uint32_t G,
+k_dist_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Params p, OwnerRule orl,
                uint32_t nchunks, uint32_t* __restrict__ bucket_out, uint32_t* __restrict__ ghist,
                DevStatus* __restrict__ st) {
     __shared__ uint32_t h[kMaxRanks];
@@ -31,6 +50,7 @@ k_dist_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Pa
     const uint64_t base = (uint64_t)blockIdx.x * kRadixChunk;
     uint32_t tl = 0, th = 0;
     constexpr int G8 = 8;
+    KeyT xs[G8];
 #pragma unroll 1
     for (int g = 0; g < kRadixItems / G8; ++g) {
         float u[G8], ul[G8];
@@ -47,6 +67,7 @@ k_dist_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Pa
                 tl += (double)x < p.lo_d;
                 th += (double)x > p.hi_d;
             }
+            xs[q] = x;
             key_to_u<KeyT>(x, p, u[q], ul[q]);
         }
         gvm_forward_fxp<MPAD, PRED, G8>(fw, u, ul, y);
@@ -56,7 +77,7 @@ k_dist_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Pa
             if (e < n) {
                 const uint32_t b = bucket_of_fxp(y[q], p.bm);
                 bucket_out[e] = b;
-                atomicAdd(&h[owner_of(b, B, G)], 1u);
+                atomicAdd(&h[owner_rule<KeyT>(orl, xs[q], b)], 1u);
             }
         }
     }
@@ -67,20 +88,21 @@ k_dist_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Pa
         if (tl) atomicAdd(&st->tail_lo, (unsigned long long)tl);
         if (th) atomicAdd(&st->tail_hi, (unsigned long long)th);
     }
-    for (uint32_t d = tid; d < G; d += kRadixThreads) ghist[(size_t)d * nchunks + blockIdx.x] = h[d];
+    for (uint32_t d = tid; d < orl.G; d += kRadixThreads) ghist[(size_t)d * nchunks + blockIdx.x] = h[d];
 }
 
 // stable scatter by owner (warp w owns elements [w*512, (w+1)*512) of the chunk, lane order)
 template <typename KeyT>
 __global__ void __launch_bounds__(kRadixThreads)
 k_dist_scatter(const KeyT* __restrict__ keys, const uint32_t* __restrict__ bucket, uint64_t n, uint64_t gofs,
-               uint64_t B, uint32_t G, uint32_t nchunks, const uint32_t* __restrict__ ghist,
+               OwnerRule orl, uint32_t nchunks, const uint32_t* __restrict__ ghist,
                KeyT* __restrict__ rkeys, uint32_t* __restrict__ rbucket, uint32_t* __restrict__ ridx) {
     constexpr int W = kRadixThreads / 32;
     __shared__ uint16_t wcnt[W][kMaxRanks];
     __shared__ uint32_t goff[kMaxRanks];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < W * (int)kMaxRanks; i += kRadixThreads) (&wcnt[0][0])[i] = 0;
+    const uint32_t G = orl.G;
     for (uint32_t d = threadIdx.x; d < G; d += kRadixThreads) goff[d] = ghist[(size_t)d * nchunks + blockIdx.x];
     __syncthreads();
     const uint64_t base = (uint64_t)blockIdx.x * kRadixChunk + (uint64_t)warp * 32 * kRadixItems;
@@ -90,7 +112,7 @@ k_dist_scatter(const KeyT* __restrict__ keys, const uint32_t* __restrict__ bucke
     for (int r = 0; r < kRadixItems; ++r) {
         const uint64_t e = base + (uint64_t)r * 32 + lane;
         const bool ok = e < n;
-        dig[r] = ok ? owner_of(bucket[e], B, G) : kMaxRanks + lane;
+        dig[r] = ok ? owner_rule<KeyT>(orl, keys[e], bucket[e]) : kMaxRanks + lane;
         const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
         const uint32_t before = ok ? wcnt[warp][dig[r]] : 0u;
         rank[r] = before + __popc(peers & lt);
@@ -121,18 +143,22 @@ k_dist_scatter(const KeyT* __restrict__ keys, const uint32_t* __restrict__ bucke
 }
 
 template <typename KeyT>
-int dist_partition(const KeyT* keys, uint64_t n, uint64_t gofs, uint64_t B, uint32_t G, uint32_t mpad, int pred,
+int dist_partition(const KeyT* keys, uint64_t n, uint64_t gofs, const OwnerRule& orl, uint32_t mpad, int pred,
                    const FoldedWeights& fw, const K1Params& kp, KeyT* rkeys, uint32_t* rbucket, uint32_t* ridx,
                    uint32_t* bucket_tmp, uint32_t* ghist, DevStatus* st, uint64_t* h_counts, cudaStream_t s) {
     const uint32_t nchunks = (uint32_t)((n + kRadixChunk - 1) / kRadixChunk);
+    const uint32_t G = orl.G;
 #define DCASE(M)                                                                                          \
     if (mpad == M) {                                                                                      \
         if (pred == kPredMufu)                                                                            \
-            k_dist_predict<KeyT, M, kPredMufu><<<nchunks, kRadixThreads, 0, s>>>(keys, n, fw, kp, B, G, nchunks, \
+            k_dist_predict<KeyT, M, kPredMufu><<<nchunks, kRadixThreads, 0, s>>>(keys, n, fw, kp, orl, nchunks, \
                                                                                   bucket_tmp, ghist, st); \
-        else                                                                                              \
-            k_dist_predict<KeyT, M, kPredMixed><<<nchunks, kRadixThreads, 0, s>>>(keys, n, fw, kp, B, G, nchunks, \
+        else if (pred == kPredMixed)                                                                      \
+            k_dist_predict<KeyT, M, kPredMixed><<<nchunks, kRadixThreads, 0, s>>>(keys, n, fw, kp, orl, nchunks, \
                                                                                    bucket_tmp, ghist, st); \
+        else                                                                                              \
+            k_dist_predict<KeyT, M, kPredPacked><<<nchunks, kRadixThreads, 0, s>>>(keys, n, fw, kp, orl, nchunks, \
+                                                                                    bucket_tmp, ghist, st); \
     }
     DCASE(16) DCASE(32) DCASE(64)
 #undef DCASE
@@ -141,7 +167,7 @@ int dist_partition(const KeyT* keys, uint64_t n, uint64_t gofs, uint64_t B, uint
     std::vector<uint32_t> h((size_t)G * nchunks);
     if (cudaMemcpyAsync(h.data(), ghist, h.size() * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return MLSORT_ERR_CUDA;
     k_radix_scan<<<1, 1024, 0, s>>>(ghist, (uint64_t)G * nchunks);
-    k_dist_scatter<KeyT><<<nchunks, kRadixThreads, 0, s>>>(keys, bucket_tmp, n, gofs, B, G, nchunks, ghist, rkeys,
+    k_dist_scatter<KeyT><<<nchunks, kRadixThreads, 0, s>>>(keys, bucket_tmp, n, gofs, orl, nchunks, ghist, rkeys,
                                                             rbucket, ridx);
     if (cudaGetLastError() != cudaSuccess) return MLSORT_ERR_CUDA;
     if (cudaStreamSynchronize(s) != cudaSuccess) return MLSORT_ERR_CUDA;

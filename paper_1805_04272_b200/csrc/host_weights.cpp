@@ -30,6 +30,7 @@ extern "C" const char* mlsort_status_string(int s) {
         case MLSORT_ERR_CAPACITY: return "output capacity exceeded";
         case MLSORT_ERR_TRAIN: return "degenerate training sample";
         case MLSORT_ERR_INTERNAL: return "internal error";
+        case MLSORT_ERR_NCCL: return "NCCL unavailable or failed";
         default: return "unknown status";
     }
 }

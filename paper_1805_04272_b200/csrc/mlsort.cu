@@ -1342,11 +1342,17 @@ extern "C" int mlsort_dist_partition(const void* d_shard, uint64_t n_local, uint
     Plan p;
     p.n = n_local;
     K1Params kp = k1_params(*w, p, B, dt == MLSORT_F32);
+    OwnerRule orl;
+    orl.B = B;
+    orl.G = nranks;
+    orl.keyspace = monotone(*w) ? 0u : 1u;    // reading A14: no bucket order without Eq. 4
+    orl.lo = w->lo;
+    orl.scale = (double)nranks / (w->hi - w->lo);
     int rc = dt == MLSORT_F32
-                 ? dist_partition<float>((const float*)d_shard, n_local, global_offset, B, nranks, mpad, pred, fw, kp,
+                 ? dist_partition<float>((const float*)d_shard, n_local, global_offset, orl, mpad, pred, fw, kp,
                                          (float*)d_rec_keys, d_rec_bucket, d_rec_index, bucket_tmp, ghist, dst,
                                          h_send_counts, s)
-                 : dist_partition<double>((const double*)d_shard, n_local, global_offset, B, nranks, mpad, pred, fw,
+                 : dist_partition<double>((const double*)d_shard, n_local, global_offset, orl, mpad, pred, fw,
                                           kp, (double*)d_rec_keys, d_rec_bucket, d_rec_index, bucket_tmp, ghist, dst,
                                           h_send_counts, s);
     if (rc) return rc;
@@ -1357,6 +1363,7 @@ extern "C" int mlsort_dist_partition(const void* d_shard, uint64_t n_local, uint
         info->tail_lo = hs->tail_lo;
         info->tail_hi = hs->tail_hi;
         info->kernel_launches = 3;
+        info->fallback_used = (int32_t)orl.keyspace;
     }
     if (hs->bad_index != ~0ull) {
         if (info) info->bad_index = (int64_t)hs->bad_index;
