@@ -1,19 +1,23 @@
 #!/usr/bin/env python3
 """bench.py -- keys/s of Machine Learning Sort on B200 (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
 N=1: the workload is BASELINE configs[1] (C2: 2^26 float32 keys ~ N(0,1), seed 2, 1->32->1
 net trained on a 2^16-key sample, B = N, key-only).  One step = one full mlsort_sort call
 (K1 predict+partition, K2, K3, K4, K5 and the status read) on device-resident keys.  The
-keys (256 MiB) are larger than the 126 MB L2, so no explicit L2 flush is needed.
+keys (256 MiB) are larger than the 126 MB L2, so no explicit L2 flush is needed.  The
+trained weights are the committed workloads/weights/<config>.json (training is a host step
+outside the timed path).
 
-N>1 (torchrun, one rank per GPU, NCCL): weak scaling, each rank holds a C2-shaped shard of
-2^26 keys of one global array of N*2^26 keys (B = global N); a step is dist_partition
-(predict + owner partition) -> NCCL all-to-all -> sort_records on every rank.
+N>1 (torchrun, one rank per GPU): BASELINE configs[3] (C4: 2^30 f32 mixture keys, M=64,
+uint32 index payload) sharded over the N GPUs -- strong scaling, total work fixed -- unless
+--config names another config (C3 at 2, C5 at 8; C2 runs weak, 2^26 keys per rank).  One
+step = one collective mlsort_sort_dist call: predict + owner partition, the library's NCCL
+all-to-all-v, the local sort and the cross-rank order check.
 
 --impl reference: the CPU oracle (oracle/, the plain fp64 implementation of the paper's
-algorithm) timed on this host's cores on a bounded sample of the same workload.
+algorithm, the only "reference" this paper has) on this host's cores, on the same config.
 
 Prints ONE JSON line (rank 0).
 """
@@ -111,70 +115,136 @@ def make_inputs(cfg, n=None, start=0):
     return keys
 
 
-def train_weights(mls, cfg):
-    # the sample: N0 keys drawn without replacement; for the full config the paper's
-    # draw over the whole array is used; training is a host step, untimed
-    keys = workloads.generate_config(cfg)
-    sample = workloads.draw_sample(keys, cfg.n0, cfg.sample_seed)
-    return mls.Weights.fit(sample, m=cfg.m, seed=cfg.train_seed), keys
+def load_weights(mls, cfg):
+    """The config's committed trained weights (scripts/make_weights.py; data, not timed)."""
+    return mls.Weights.load(workloads.weights_path(cfg.name))
 
 
-def cpu_baseline(cfg, weights_params, sample_keys):
-    """The oracle as it stands (single-threaded C, fp64) on a bounded sample."""
+def host_info():
+    cpu = ""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                cpu = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": cpu}
+
+
+PAPER_CONTEXT = ("P:103, single CPU (model unstated), 10^7 doubles: Python sorted 10 s (1.0 Mkeys/s), "
+                 "NumPy quicksort 0.9 s (11.1 Mkeys/s), NumPy mergesort 2 s (5.0 Mkeys/s); MLsort times "
+                 "only in the lost Fig. 3 -- context, not a target")
+
+
+def cpu_baseline(cfg, keys):
+    """SURVEY.md §8(d) CPU baselines on this host: the oracle as it stands (its own step
+    functions in the paper's order) on the full config, single-threaded with per-phase times
+    and with nproc threads on the predict step; the full C1 config single-threaded; predict
+    alone with nproc threads on 2^24-key samples of C1-C5; std::sort / std::stable_sort on
+    1 thread over the same keys."""
     import oracle
+    hi = host_info()
+    T = hi["nproc"] or 1
+    w = workloads.load_weights_dict(cfg.name)
+    out = {"unit": "keys/s", "kind": "oracle", "host": hi, "paper_context": PAPER_CONTEXT}
     t0 = time.perf_counter()
-    r = oracle.ml_sort(sample_keys, weights_params, B=len(sample_keys))
-    dt = time.perf_counter() - t0
-    ok = bool(np.all(np.diff(oracle.order_bits(r["keys"]).astype(np.int64)) >= 0))
-    return {"value": len(sample_keys) / dt, "unit": "keys/s", "cores": 1, "kind": "oracle",
-            "sample": f"{len(sample_keys)} keys of {cfg.name} ({cfg.dist}, seed {cfg.seed}), B = sample size, "
-                      f"M={cfg.m}, {dt:.2f} s single-threaded", "verified_sorted": ok}
+    r = oracle.ml_sort_phased(keys, w, B=cfg.buckets, threads=T)
+    tT = time.perf_counter() - t0
+    out.update({"value": cfg.n / tT, "cores": T,
+                "sample": f"the full {cfg.name} config ({cfg.n} keys), oracle with {T} threads on the "
+                          f"predict step, every other step sequential; {tT:.1f} s",
+                "phase_s_threads": {k: round(v, 3) for k, v in r["phase_s"].items()}})
+    del r
+    t0 = time.perf_counter()
+    r = oracle.ml_sort_phased(keys, w, B=cfg.buckets, threads=1)
+    t1 = time.perf_counter() - t0
+    out["single_thread"] = {"value": cfg.n / t1, "seconds": round(t1, 2),
+                            "phase_s": {k: round(v, 3) for k, v in r["phase_s"].items()}}
+    del r
+    c1 = workloads.CONFIGS["C1"]
+    k1 = workloads.generate_config(c1)
+    t0 = time.perf_counter()
+    r = oracle.ml_sort_phased(k1, workloads.load_weights_dict("C1"), B=c1.buckets, threads=1)
+    t1 = time.perf_counter() - t0
+    out["C1_single_thread"] = {"value": c1.n / t1, "seconds": round(t1, 3),
+                               "phase_s": {k: round(v, 4) for k, v in r["phase_s"].items()}}
+    pred = {}
+    for name in ("C1", "C2", "C3", "C4", "C5"):
+        c = workloads.CONFIGS[name]
+        ks = workloads.generate_config(c, n=min(c.n, 1 << 24))
+        wd = workloads.load_weights_dict(name)
+        t0 = time.perf_counter()
+        oracle.ml_sort_phased(ks[:4096], wd, threads=1)          # (warm the library)
+        bounds = [(i * len(ks)) // T for i in range(T + 1)]
+        from concurrent.futures import ThreadPoolExecutor
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(T) as ex:
+            list(ex.map(lambda i: oracle.predict(wd, ks[bounds[i]:bounds[i + 1]]), range(T)))
+        dt = time.perf_counter() - t0
+        pred[name] = {"keys": len(ks), "keys_per_s": len(ks) / dt, "activations_per_s": len(ks) * c.m / dt}
+    out["predict_nproc_threads"] = pred
+    for stable in (False, True):
+        t0 = time.perf_counter()
+        oracle.std_sort(keys, stable)
+        dt = time.perf_counter() - t0
+        out["std_stable_sort_1t" if stable else "std_sort_1t"] = {"value": cfg.n / dt, "seconds": round(dt, 2)}
+    return out
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle is the reference arm (no reference code exists)."""
+    """--impl reference: the CPU oracle is the reference arm (no reference code exists).  Each
+    timed step sorts the FULL config with the oracle's own step functions in the paper's order
+    (ml_sort_phased), the predict step spread over this host's cores; warm-up steps run on a
+    2^20-key slice (no JIT to warm on the CPU).  The product library is never loaded."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
-    import paper_1805_04272_b200 as mls
-    cfg = workloads.CONFIGS[args.config]
-    # bounded per-step sample so W+K steps finish within a few minutes
-    ns = args.ref_sample
-    keys = workloads.generate_config(cfg, n=ns)
-    w = mls.Weights.fit(workloads.draw_sample(keys, min(cfg.n0, ns // 4), cfg.sample_seed), m=cfg.m,
-                        seed=cfg.train_seed)
-    p = w.params()
+    cfg = workloads.CONFIGS[args.config or "C2"]
+    keys = workloads.generate_config(cfg)
+    w = workloads.load_weights_dict(cfg.name)
+    T = os.cpu_count() or 1
     for _ in range(args.warmup):
-        oracle.ml_sort(keys, p)
-    times = []
+        oracle.ml_sort_phased(keys[:1 << 20], w, threads=T)
+    times, phases = [], None
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.ml_sort(keys, p)
+        r = oracle.ml_sort_phased(keys, w, B=cfg.buckets, threads=T)
         times.append(time.perf_counter() - t0)
+        phases = r["phase_s"]
+        del r
     tot = sum(times)
-    value = ns * args.steps / tot
+    value = cfg.n * args.steps / tot
+    sample = (f"the full {cfg.name} config ({cfg.n} keys) per step; oracle with {T} threads on the predict "
+              f"step, every other step sequential")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"{cfg.name} sample", "n": ns, "dist": cfg.dist,
-                                             "m": cfg.m, "buckets": "n"},
-            "cpu_baseline": {"value": value, "unit": "keys/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{ns} keys of {cfg.name} per step, single-threaded fp64 oracle"},
+            "data": "synthetic", "config": {"workload": config_name(cfg), "n": cfg.n, "buckets": cfg.buckets,
+                                             "m": cfg.m, "same_config": True},
+            "cpu_baseline": {"value": value, "unit": "keys/s", "cores": T, "kind": "oracle", "sample": sample,
+                             "host": host_info(), "phase_s_last_step": {k: round(v, 3) for k, v in phases.items()}},
             "e2e": {"value": value, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def config_name(cfg):
+    return (f"{cfg.name}: 2^{int(math.log2(cfg.n))} {cfg.dtype} {cfg.dist} seed {cfg.seed}, "
+            f"1->{cfg.m}->1 net trained on a {cfg.n0}-key sample, B={cfg.buckets}, "
+            f"{'stable+perm' if cfg.perm else 'key-only'}")
 
 
 def run_single(args):
     import torch
     import paper_1805_04272_b200 as mls
-    cfg = workloads.CONFIGS[args.config]
+    cfg = workloads.CONFIGS[args.config or "C2"]
     torch.cuda.set_device(0)
-    w, keys = train_weights(mls, cfg)
-    p = w.params()
+    w = load_weights(mls, cfg)
+    keys = workloads.generate_config(cfg)
     dt_keys = torch.float32 if cfg.dtype == "f32" else torch.float64
     d_keys = torch.from_numpy(keys).cuda()
-    pred = {"mufu": 1, "mixed": 2, "packed": 3, "default": 0}[args.predictor]
+    pred = {"mufu": 1, "mixed": 2, "packed": 3, "skip": 4, "default": 0}[args.predictor]
     sorter = mls.Sorter(cfg.n, dt_keys, cfg.perm, cfg.buckets, pred, timing=True).bind(w)
     out_k = torch.empty_like(d_keys)
     out_p = torch.empty(cfg.n, dtype=torch.int32, device="cuda") if cfg.perm else None
@@ -236,6 +306,9 @@ def run_single(args):
             traffic = json.load(open(tf)).get(cfg.name)
         except Exception:
             traffic = None
+    # K1 variant the plan ran (k1_ws = warp-specialized predict + partition; "grouped" = value
+    # grouping with saturated-pair skipping, MLSORT_PRED_SKIP, the default for M > 32)
+    k1_name = "k1_ws" + (" (grouped)" if (pred == 4 or (pred == 0 and cfg.m > 32)) else "")
     # whole-step roofline: max(SFU time, HBM time of 2*s_k (+4) bytes/key)
     alg_bytes = cfg.n * (2 * ks + (4 if cfg.perm else 0))
     t_roof = max(acts / (peak_act * 1e9), alg_bytes / (pk["hbm_gbs"] * 1e9))
@@ -246,13 +319,11 @@ def run_single(args):
         "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: 2^{int(math.log2(cfg.n))} {cfg.dtype} {cfg.dist} seed {cfg.seed}, "
-                               f"1->{cfg.m}->1 net trained on a {cfg.n0}-key sample, B={cfg.buckets}, "
-                               f"{'stable+perm' if cfg.perm else 'key-only'}",
+        "config": {"workload": config_name(cfg),
                    "n": cfg.n, "buckets": cfg.buckets, "m": cfg.m, "predictor": args.predictor,
                    "l2": "inputs (%d MiB) larger than L2 (126 MB); no flush" % (cfg.n * ks >> 20),
                    "parallelism": "1 GPU"},
-        "roofline": {"bound": "alu", "kernel": "k1_predict_partition", "achieved": achieved, "peak": peak_act,
+        "roofline": {"bound": "alu", "kernel": k1_name, "achieved": achieved, "peak": peak_act,
                      "unit": "Gact/s", "frac": achieved / peak_act, "traffic": traffic,
                      "peak_source": f"derived: {SMS} SMs x {MUFU_PER_CLK_PER_SM} MUFU/clk x "
                                     f"{pk['sm_max_mhz']:.0f} MHz (1 MUFU.EX2 per activation)",
@@ -268,53 +339,53 @@ def run_single(args):
                                          "tail_lo", "tail_hi")},
     }
     if not args.no_cpu_baseline:
-        ns = args.cpu_sample
-        sk = workloads.generate_config(cfg, n=ns)
-        line["cpu_baseline"] = cpu_baseline(cfg, p, sk)
+        line["cpu_baseline"] = cpu_baseline(cfg, keys)
     print(json.dumps(line), flush=True)
 
 
 def run_multi(args):
+    """N>1: one rank per GPU; a step is one collective mlsort_sort_dist call (library NCCL)."""
     import torch
     import torch.distributed as dist
     import paper_1805_04272_b200 as mls
-    from paper_1805_04272_b200 import dist as mdist
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    base = workloads.CONFIGS[args.config]
-    per = base.n
-    n_global = per * world
-    B = n_global
-    keys = workloads.generate(base.dist, per, base.seed, base.dtype, start=rank * per, **base.params)
-    # every rank fits the same weights from the same n0 keys (iid draws: any n0 keys are a
-    # uniform sample of the population), deterministic across ranks
-    sample = workloads.generate(base.dist, base.n0, base.seed + 7777, base.dtype, **base.params)
-    w = mls.Weights.fit(sample, m=base.m, seed=base.train_seed)
+    base = workloads.CONFIGS[args.config or "C4"]
+    weak = base.name == "C2"
+    n_global = base.n * world if weak else base.n
+    B = n_global if weak else base.buckets
+    lo_i, hi_i = (rank * n_global) // world // 4 * 4, ((rank + 1) * n_global) // world // 4 * 4
+    if rank == world - 1:
+        hi_i = n_global
+    n_local = hi_i - lo_i
+    keys = workloads.generate(base.dist, n_local, base.seed, base.dtype, start=lo_i, **base.params)
+    w = load_weights(mls, base)
     d_keys = torch.from_numpy(keys).cuda()
-    part = mdist.cuda_partition_fn(w)
-    lsort = mdist.cuda_local_sort_fn()
+    comm = mls.Comm(device=torch.device("cuda", local))
+    cap = int(n_global / world * 1.25) + (1 << 20)
+    kw = dict(perm=base.perm, num_buckets=B, timing=True)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
-        mdist.sort_dist(d_keys, rank * per, n_global, B, part, lsort, with_index=base.perm)
+        k, i, goff, info = comm.sort(d_keys, w, lo_i, n_global, capacity=cap, **kw)
+        cap = max(cap, comm.last[0].numel())
     torch.cuda.synchronize()
-    dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a2a = []
-    l0 = part.launches + lsort.launches
+    a2a, launches = [], 0
     with ClockSampler(local) as clk:
         dist.barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            res = mdist.sort_dist(d_keys, rank * per, n_global, B, part, lsort, with_index=base.perm)
-            a2a.append(res.exchange_ms)
+            k, i, goff, info = comm.sort(d_keys, w, lo_i, n_global, capacity=cap, out_keys=comm.last[0],
+                                         out_perm=comm.last[1], workspace=comm.last[2], **kw)
+            a2a.append(float(info.phase_ms[2]))
+            launches += int(info.kernel_launches)
         ev1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
-    launches = part.launches + lsort.launches - l0
     ms = ev0.elapsed_time(ev1) / args.steps
     t = torch.tensor([ms, statistics.mean(a2a)], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -322,19 +393,22 @@ def run_multi(args):
     # end to end through the same public API from pinned host memory: H2D of the shard, the
     # distributed sort, D2H of this rank's sorted run (and its global indices)
     h_keys = torch.from_numpy(keys).pin_memory()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h_out = torch.empty(cap, dtype=d_keys.dtype).pin_memory()
+    h_idx = torch.empty(cap, dtype=torch.int32).pin_memory() if base.perm else None
     dist.barrier()
     torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     d2h = 0
     for _ in range(args.steps):
-        dk = h_keys.to("cuda", non_blocking=True)
-        r = mdist.sort_dist(dk, rank * per, n_global, B, part, lsort, with_index=base.perm)
-        hk = r.keys.to("cpu")
-        d2h = hk.numel() * hk.element_size()
-        if r.index is not None:
-            hi = r.index.to("cpu")
-            d2h += hi.numel() * hi.element_size()
+        d_keys.copy_(h_keys, non_blocking=True)
+        k, i, goff, info = comm.sort(d_keys, w, lo_i, n_global, capacity=cap, out_keys=comm.last[0],
+                                     out_perm=comm.last[1], workspace=comm.last[2], **kw)
+        h_out[:k.numel()].copy_(k, non_blocking=True)
+        d2h = k.numel() * k.element_size()
+        if i is not None:
+            h_idx[:i.numel()].copy_(i, non_blocking=True)
+            d2h += i.numel() * 4
     e1.record(stream)
     torch.cuda.synchronize()
     t2 = torch.tensor([e0.elapsed_time(e1) / args.steps, float(d2h)], device="cuda")
@@ -343,26 +417,30 @@ def run_multi(args):
     ks = 4 if base.dtype == "f32" else 8
     pk = peaks()
     peak_act = SMS * MUFU_PER_CLK_PER_SM * pk["sm_max_mhz"] * 1e6 / 1e9
-    acts = n_global * base.m
-    achieved = acts / (ms_max * 1e-3) / 1e9 / world          # per GPU
+    achieved = n_global * base.m / (ms_max * 1e-3) / 1e9 / world          # per GPU
+    nvl_bytes = n_global / world * (world - 1) / world * (ks + 4 + (4 if base.perm else 0))
     if rank == 0:
         line = {"metric": METRIC, "value": n_global / (ms_max * 1e-3), "unit": "keys/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": base.dtype, "data": "synthetic",
-                "config": {"workload": f"{base.name}-shaped shard of 2^{int(math.log2(per))} keys per rank, "
-                                       f"global N={n_global}, B=N, rank-range all-to-all (NCCL)",
-                           "parallelism": f"dp{world}", "n_global": n_global,
+                "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": base.dtype,
+                "data": "synthetic",
+                "config": {"workload": (f"{base.name}-shaped shard of 2^{int(math.log2(base.n))} keys per rank"
+                                        if weak else config_name(base) + f", sharded over {world} GPUs"),
+                           "parallelism": f"dp{world} (rank-range all-to-all, library-owned NCCL)",
+                           "n_global": n_global, "buckets": B,
                            "l2": "inputs larger than L2 (126 MB); no flush"},
                 "roofline": {"bound": "alu", "kernel": "whole step per GPU (predict dominates)",
                              "achieved": achieved, "peak": peak_act, "unit": "Gact/s", "frac": achieved / peak_act,
                              "traffic": None, "all_to_all_ms": a2a_max,
+                             "all_to_all_records_bytes_per_rank": nvl_bytes,
                              "peak_source": f"derived: {SMS} SMs x {MUFU_PER_CLK_PER_SM} MUFU/clk x "
                                             f"{pk['sm_max_mhz']:.0f} MHz"},
                 "e2e": {"value": n_global / (e2e_ms * 1e-3), "unit": "keys/s",
-                        "h2d_bytes_per_step": per * ks * world, "d2h_bytes_per_step": int(t2[1].item()) * world,
+                        "h2d_bytes_per_step": n_global * ks, "d2h_bytes_per_step": int(t2[1].item()) * world,
                         "ms_per_step": e2e_ms},
                 "clocks": clk.summary(), "gpu_launches": launches}
         print(json.dumps(line), flush=True)
+    comm.close()
     dist.destroy_process_group()
 
 
@@ -372,16 +450,18 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--predictor", default="default", choices=["default", "mufu", "mixed", "packed"])
-    ap.add_argument("--cpu-sample", type=int, default=1 << 21)
-    ap.add_argument("--ref-sample", type=int, default=1 << 20)
+    ap.add_argument("--config", default=None, help="C1..C5 (default: C2 at N=1, C4 sharded at N>1)")
+    ap.add_argument("--predictor", default="default", choices=["default", "mufu", "mixed", "packed", "skip"])
+    ap.add_argument("--dist", action="store_true", help="run the mlsort_sort_dist path even at N=1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
         return
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.dist:
+        if "RANK" not in os.environ:            # --dist at N=1 without torchrun
+            os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0", "MASTER_ADDR": "127.0.0.1",
+                               "MASTER_PORT": os.environ.get("MASTER_PORT", "29517")})
         run_multi(args)
     else:
         run_single(args)

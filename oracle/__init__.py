@@ -30,15 +30,42 @@ _lib = None
 ORACLE_ERR_NONFINITE = 5
 
 
+_BASE_SRC = os.path.join(_HERE, "cpu_baselines.cpp")
+_BASE_LIB = os.path.join(_HERE, "libcpubase.so")
+_base = None
+
+
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (no fast-math, no FMA contraction)."""
+    """Compile the oracle with gcc (no fast-math, no FMA contraction), and the conventional
+    CPU sorts of the bench's cpu_baseline (std::sort / std::stable_sort)."""
     if force or not os.path.exists(_LIB_PATH) or \
             os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
                                "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB_PATH)
+    if force or not os.path.exists(_BASE_LIB) or \
+            os.path.getmtime(_BASE_LIB) < os.path.getmtime(_BASE_SRC):
+        tmp = _BASE_LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", tmp, _BASE_SRC])
+        os.replace(tmp, _BASE_LIB)
     return _LIB_PATH
+
+
+def std_sort(keys, stable: bool = False) -> np.ndarray:
+    """std::sort / std::stable_sort (1 thread) of a copy of the keys: a conventional baseline
+    (SURVEY.md §8(d)), not part of the oracle's algorithm."""
+    global _base
+    if _base is None:
+        build()
+        _base = C.CDLL(_BASE_LIB)
+        for f in (_base.cpu_std_sort_f32, _base.cpu_std_sort_f64):
+            f.argtypes = [C.c_void_p, C.c_uint64, C.c_int]
+            f.restype = None
+    a = np.array(keys, copy=True)
+    fn = _base.cpu_std_sort_f32 if a.dtype == np.float32 else _base.cpu_std_sort_f64
+    fn(a.ctypes.data_as(C.c_void_p), a.shape[0], 1 if stable else 0)
+    return a
 
 
 def _load():
@@ -192,6 +219,55 @@ def ml_sort(keys, w: dict, B: int = 0, stable: bool = True, want_y: bool = False
     if want_counts:
         out["counts"] = cnt[:B] if n else np.zeros(B, dtype=np.uint32)
     return out
+
+
+def ml_sort_phased(keys, w: dict, B: int = 0, threads: int = 1, stable: bool = True) -> dict:
+    """The same pipeline as ml_sort -- the oracle's own step functions called in the paper's
+    order (validate, predict Eq. 3, bucket, tails, place + fix-up, verify/repair) -- with a
+    wall time per phase.  Step 2 (predict, independent per key: P:94) may run on `threads`
+    host threads over contiguous chunks (ctypes releases the GIL); every other step is the
+    sequential C code.  The output is identical to ml_sort (pinned in test_oracle_pins)."""
+    import time
+    from concurrent.futures import ThreadPoolExecutor
+    keys = np.asarray(keys)
+    x = _as_f64(keys)
+    n = x.shape[0]
+    B = int(B) if B else n
+    ph = {}
+    t0 = time.perf_counter()
+    bad = validate(x)                                                   # step 1
+    ph["validate"] = time.perf_counter() - t0
+    if bad >= 0:
+        raise NonFiniteKey(bad)
+    t0 = time.perf_counter()
+    if threads <= 1 or n < 4096:
+        y = predict(w, x)                                               # step 2
+    else:
+        y = np.empty(n, dtype=np.float64)
+        m, (w1, w2, b_, beta), lo, hi = _weights(w)
+        bounds = [(i * n) // threads for i in range(threads + 1)]
+
+        def part(i):
+            a, e = bounds[i], bounds[i + 1]
+            _load().oracle_predict(m, _ptr(w1), _ptr(w2), _ptr(b_), _ptr(beta), lo, hi,
+                                   C.c_void_p(x.ctypes.data + 8 * a), e - a, C.c_void_p(y.ctypes.data + 8 * a))
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(part, range(threads)))
+    ph["predict"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    bk = bucket(y, B)                                                   # step 3
+    ph["bucket"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    tl, th = tails(x, w["input_lo"], w["input_hi"])                     # step 4
+    ph["tails"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ok, oi, cnt, moves = place_fixup(x, bk, B)                          # steps 5-7
+    ph["place_fixup"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ok, oi, rep = verify_repair(ok, oi, stable)                         # step 8
+    ph["verify"] = time.perf_counter() - t0
+    return {"keys": ok.astype(keys.dtype) if keys.dtype != np.float64 else ok, "perm": oi, "repairs": rep,
+            "tail_lo": tl, "tail_hi": th, "phase_s": ph, "threads": threads}
 
 
 def expected_occupancy(N: int, B: int, q: int) -> float:

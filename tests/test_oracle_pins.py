@@ -355,3 +355,25 @@ def test_sorted_reference_matches_stable_argsort(dist, dt):
     ref = np.argsort(oracle.order_bits(keys), kind="stable")
     np.testing.assert_array_equal(perm, ref.astype(np.uint32))
     np.testing.assert_array_equal(sk.view(np.uint8), keys[ref].view(np.uint8))
+
+
+@pytest.mark.parametrize("threads", [1, 3])
+@pytest.mark.parametrize("dist,dt", [("normal", "f32"), ("lognormal", "f64"), ("grid4096", "f32")])
+def test_ml_sort_phased_equals_ml_sort(threads, dist, dt):
+    """The phased / threaded composition (bench cpu_baseline and --impl reference) returns
+    exactly ml_sort's output: same steps, same order, predict split by key only."""
+    keys = workloads.generate(dist, 50001, 4, dt)
+    s = workloads.draw_sample(keys, 2000, 1)
+    w = workloads.random_monotone_weights(10, 2, lo=float(s.min()), hi=float(s.max()), scale=5.0)
+    a = oracle.ml_sort(keys, w, B=40000)
+    b = oracle.ml_sort_phased(keys, w, B=40000, threads=threads)
+    np.testing.assert_array_equal(a["perm"], b["perm"])
+    np.testing.assert_array_equal(a["keys"].view(np.uint8), b["keys"].view(np.uint8))
+    assert (a["repairs"], a["tail_lo"], a["tail_hi"]) == (b["repairs"], b["tail_lo"], b["tail_hi"])
+    assert set(b["phase_s"]) == {"validate", "predict", "bucket", "tails", "place_fixup", "verify"}
+
+
+def test_std_sort_baseline_sorts():
+    keys = workloads.generate("normal", 100000, 3, "f32")
+    for stable in (False, True):
+        np.testing.assert_array_equal(oracle.std_sort(keys, stable), np.sort(keys))
