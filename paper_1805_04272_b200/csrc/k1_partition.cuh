@@ -34,12 +34,17 @@ struct K1Params {
     uint32_t capc;           // region capacity (elements) of every coarse bucket
     uint64_t n;
     uint32_t tile0;          // first tile of this launch (chunked launches overlap the H2D copy)
+    // u is clamped into [u_cl_lo, u_cl_hi] (+-inf: no clamp).  Beyond these bounds EVERY neuron is
+    // saturated, where each term of the packed predictor is an exact constant (DESIGN.md "K1
+    // sparse evaluation"), so the clamp changes no output bit; inside them no logistic argument
+    // exceeds 120, so the predictor needs no per-activation clamp (FoldedWeights::u_safe_*).
+    float u_cl_lo, u_cl_hi;
     uint32_t pad0;
 };
 
 template <typename KeyT> __device__ __forceinline__ void key_to_u(KeyT x, const K1Params& p, float& uh, float& ul);
 template <> __device__ __forceinline__ void key_to_u<float>(float x, const K1Params& p, float& uh, float& ul) {
-    uh = x - p.x0_f;
+    uh = fminf(fmaxf(x - p.x0_f, p.u_cl_lo), p.u_cl_hi);
     ul = 0.0f;
 }
 // f64 keys: u = x - x0 in f64, rounded once to f32.  y then depends on x only through the
@@ -48,7 +53,7 @@ template <> __device__ __forceinline__ void key_to_u<float>(float x, const K1Par
 // at most |u dy/du| 2^-24 <~ 1e-7 of y.  Keys closer than one f32 ulp of u
 // share a rank bucket; the fix-up orders them by the full f64 key.
 template <> __device__ __forceinline__ void key_to_u<double>(double x, const K1Params& p, float& uh, float& ul) {
-    uh = (float)(x - p.x0_d);
+    uh = fminf(fmaxf((float)(x - p.x0_d), p.u_cl_lo), p.u_cl_hi);
     ul = 0.0f;
 }
 

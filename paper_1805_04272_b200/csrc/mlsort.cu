@@ -217,6 +217,34 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
     f.u_safe_lo = ulo == -INFINITY ? -INFINITY : (float)std::nextafter((float)ulo, INFINITY);
     f.u_safe_hi = uhi == INFINITY ? INFINITY : (float)std::nextafter((float)uhi, -INFINITY);
     if (!(f.u_safe_lo <= f.u_safe_hi)) { f.u_safe_lo = INFINITY; f.u_safe_hi = -INFINITY; }
+    // ---- key-side clamp (K1Params u_cl_lo/hi): below min_p lo2[p] every pair is in its left
+    // saturation and above max_p hi2[p] in its right one, where each term is an exact constant;
+    // clamping u just inside those bounds changes no output bit.  If no argument can exceed
+    // kANoClamp inside them, every warp runs the clamp-free chain.
+    f.u_cl_lo = -INFINITY;
+    f.u_cl_hi = INFINITY;
+    {
+        float lo = INFINITY, hi = -INFINITY;
+        for (uint32_t pp = 0; pp < mpad / 2; ++pp) {
+            if (std::isfinite(f.lo2[pp])) lo = std::min(lo, f.lo2[pp]);
+            if (std::isfinite(f.hi2[pp])) hi = std::max(hi, f.hi2[pp]);
+        }
+        bool ok = std::isfinite(lo) && std::isfinite(hi) && lo <= hi;
+        if (ok) {
+            lo = std::nextafter(lo, -INFINITY);
+            hi = std::nextafter(hi, INFINITY);
+            for (uint32_t j = 0; j < mpad && ok; ++j) {
+                const double a1 = (double)f.A[j] * lo + (double)f.Cs[j], a2 = (double)f.A[j] * hi + (double)f.Cs[j];
+                ok = std::max(a1, a2) <= (double)kANoClamp - 1.0;
+            }
+        }
+        if (ok && !std::getenv("MLSORT_NO_UCLAMP")) {
+            f.u_cl_lo = lo;
+            f.u_cl_hi = hi;
+            f.u_safe_lo = -INFINITY;
+            f.u_safe_hi = INFINITY;
+        }
+    }
     auto pair = [](float v) {
         uint32_t bb;
         std::memcpy(&bb, &v, 4);
@@ -740,8 +768,10 @@ int fallback_sort(const KeyT* keys, uint64_t n, KeyT* out_keys, uint32_t* out_pe
     return MLSORT_OK;
 }
 
-K1Params k1_params(const Weights& w, const Plan& p, uint64_t B, bool f32) {
+K1Params k1_params(const Weights& w, const Plan& p, uint64_t B, bool f32, const FoldedWeights* fw = nullptr) {
     K1Params kp;
+    kp.u_cl_lo = fw ? fw->u_cl_lo : -INFINITY;
+    kp.u_cl_hi = fw ? fw->u_cl_hi : INFINITY;
     kp.lo_d = w.lo;
     kp.hi_d = w.hi;
     kp.x0_d = origin_of(w, f32);
@@ -827,7 +857,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     if (!GIVEN) {
         mpad = mpad_of(w->m);
         fw = fold_cached(*w, mpad, sizeof(KeyT) == 4);
-        kp = k1_params(*w, p, B, sizeof(KeyT) == 4);
+        kp = k1_params(*w, p, B, sizeof(KeyT) == 4, &fw);
     } else {
         std::memset(&fw, 0, sizeof(fw));
         Weights dummy;
@@ -1263,7 +1293,7 @@ int launch_predict(const KeyT* keys, uint64_t n, const Weights& w, uint64_t B, i
     FoldedWeights fw = fold_cached(w, mpad, sizeof(KeyT) == 4);
     Plan p;
     p.n = n;
-    K1Params kp = k1_params(w, p, B, sizeof(KeyT) == 4);
+    K1Params kp = k1_params(w, p, B, sizeof(KeyT) == 4, &fw);
     const uint64_t warps = (n + 32 * 8 - 1) / (32 * 8);
     const int grid = (int)std::min<uint64_t>((uint64_t)num_sms() * 8, (warps + 7) / 8);
 #define PCASE(M)                                                                                    \
@@ -1341,7 +1371,7 @@ extern "C" int mlsort_dist_partition(const void* d_shard, uint64_t n_local, uint
     FoldedWeights fw = fold_cached(*w, mpad, dt == MLSORT_F32);
     Plan p;
     p.n = n_local;
-    K1Params kp = k1_params(*w, p, B, dt == MLSORT_F32);
+    K1Params kp = k1_params(*w, p, B, dt == MLSORT_F32, &fw);
     OwnerRule orl;
     orl.B = B;
     orl.G = nranks;

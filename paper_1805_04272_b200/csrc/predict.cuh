@@ -32,8 +32,10 @@ struct __align__(16) FoldedWeights {
     float Cs[kMaxM];
     float Wns[kMaxM];
     // u in [u_safe_lo, u_safe_hi] keeps every shifted argument A_j u + Cs_j <= kAClamp, so the
-    // packed predictor may skip its per-activation clamp for such keys (CLAMP = false)
-    float u_safe_lo, u_safe_hi, pad_f[2];
+    // packed predictor may skip its per-activation clamp for such keys (CLAMP = false).  When
+    // u_cl_lo/hi are finite, keys clamp u into [u_cl_lo, u_cl_hi] (K1Params), every argument
+    // there is <= kANoClamp and u_safe spans everything.
+    float u_safe_lo, u_safe_hi, u_cl_lo, u_cl_hi;
     // Saturated-pair skipping.  Neurons are stored sorted by
     // centre.  For u < lo2[p] both neurons of pair p have a > 24.5 or a < -26.5 on their left
     // side, and for u > hi2[p] on their right side; there the computed fixed-point terms are
@@ -129,6 +131,11 @@ constexpr uint32_t kSeedNeg = 0xFEF33400u;
 // faster (1.044 -> 1.021 ms).  Measured and kept off (s = 0, clamp at 59 -> d <= 2^60).
 constexpr float kAShift = 0.0f;
 constexpr float kAClamp = 60.0f;             // 0x7EF33400 + 0x80000000: bits of -r0 from bits(d)
+// Largest argument the chain takes without a clamp: d = 1 + 2^a <= 2^120 keeps the seed
+// 0xFEF33400 - bits(d) a negative NORMAL float and every intermediate finite; for a >= 24 the
+// term W r + magic rounds to magic exactly (|W r| < 1/4), so nothing depends on the chain's
+// accuracy there.
+constexpr float kANoClamp = 120.0f;
 
 // -1/d for both lanes of d2 (d in [1, 2^61]) by the packed chain above; shared by the predictor
 // and the exhaustive monotonicity sweep (selftest.cuh), so the swept instructions are the

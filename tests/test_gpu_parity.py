@@ -382,3 +382,34 @@ def test_f64_lognormal_large_no_fallback(mls, n, m):
     np.testing.assert_array_equal(_bits(k.cpu().numpy()), _bits(ref_keys))
     print("info", info)
     assert info["fallback_used"] == 0, info
+
+
+@pytest.mark.parametrize("name,pred", [("C2", 3), ("C2", 2), ("C4", 4), ("C4", 3), ("C3", 4), ("C5", 3)])
+def test_key_clamp_bit_identical(mls, name, pred):
+    """The key-side clamp of u (K1Params u_cl_lo/hi): beyond the
+    bounds every neuron is saturated and its term an exact constant, so clamping changes no
+    output bit.  Compared against the same weights folded with MLSORT_NO_UCLAMP=1, on keys
+    spanning the whole finite range (far tails on both sides) plus the config's own keys."""
+    import os
+    cfg = workloads.CONFIGS[name]
+    p = workloads.load_weights_dict(name)
+    w = mls.Weights.from_dict(p)
+    os.environ["MLSORT_NO_UCLAMP"] = "1"
+    try:
+        w_ref = mls.Weights.from_dict(p)
+        mls.predict(_t(np.zeros(8, dtype=np.float32 if cfg.dtype == "f32" else np.float64)), w_ref)   # fold now
+        if cfg.dtype == "f64":
+            mls.predict(_t(np.zeros(8, dtype=np.float32)), w_ref)
+    finally:
+        del os.environ["MLSORT_NO_UCLAMP"]
+    rng = np.random.default_rng(5)
+    npdt = np.float32 if cfg.dtype == "f32" else np.float64
+    big = np.finfo(np.float32).max if cfg.dtype == "f32" else 1e300
+    wide = np.sign(rng.random(1 << 18) - 0.5) * np.exp(rng.uniform(-80, np.log(big), 1 << 18))
+    keys = np.concatenate([workloads.generate_config(cfg, n=1 << 18), wide.astype(npdt),
+                           np.array([p["input_lo"], p["input_hi"], -big, big, 0.0], dtype=npdt)])
+    for B in (cfg.buckets, 1000):
+        y1, b1 = mls.predict(_t(keys), w, num_buckets=B, predictor=pred)
+        y0, b0 = mls.predict(_t(keys), w_ref, num_buckets=B, predictor=pred)
+        assert bool((y1.view(torch_int32()) == y0.view(torch_int32())).all())
+        assert bool((b1 == b0).all())
