@@ -810,15 +810,34 @@ struct ChunkPlan {
 
 // The core pipeline shared by mlsort_sort (predict) and mlsort_sort_records (GIVEN buckets).
 struct PhaseTimer {
+    // events are created once per (thread, device) and reused: creating and destroying them per
+    // call would put ~12 driver calls of host time into every timed sort
     bool on = false;
-    cudaEvent_t ev[6] = {};
+    cudaEvent_t* ev = nullptr;
     int n = 0;
     cudaStream_t s = nullptr;
     void start(bool enable, cudaStream_t st) {
-        on = enable;
+        on = false;
+        if (!enable) return;
+        struct Pool {
+            int dev;
+            cudaEvent_t ev[6];
+        };
+        thread_local std::vector<Pool> pools;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        for (auto& p : pools)
+            if (p.dev == dev) ev = p.ev;
+        if (!ev) {
+            Pool p;
+            p.dev = dev;
+            for (auto& e : p.ev)
+                if (cudaEventCreate(&e) != cudaSuccess) return;
+            pools.push_back(p);
+            ev = pools.back().ev;
+        }
+        on = true;
         s = st;
-        if (!on) return;
-        for (auto& e : ev) cudaEventCreate(&e);
         cudaEventRecord(ev[0], s);
         n = 1;
     }
@@ -831,12 +850,7 @@ struct PhaseTimer {
             for (int i = 1; i < n; ++i) cudaEventElapsedTime(&info->phase_ms[i - 1], ev[i - 1], ev[i]);
             cudaEventElapsedTime(&info->phase_ms[5], ev[0], ev[n - 1]);
         }
-        for (auto& e : ev) cudaEventDestroy(e);
         on = false;
-    }
-    ~PhaseTimer() {
-        if (on)
-            for (auto& e : ev) cudaEventDestroy(e);
     }
 };
 
@@ -875,15 +889,11 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     const unsigned long long* rbase = nullptr;   // regions at c * capc; exact layout on a retry
     const uint64_t nranges = (uint64_t)p.C * p.R;
     for (int attempt = 0;; ++attempt) {
-        {
-            DevStatus init;
-            std::memset(&init, 0, sizeof(init));
-            init.bad_index = ~0ull;
-            CK(cudaMemcpyAsync(dst, &init, sizeof(init), cudaMemcpyHostToDevice, s));
-        }
-        CK(cudaMemsetAsync(at<void>(ws, L.range_start), 0xff, (size_t)p.C * p.R * 8, s));
-        CK(cudaMemsetAsync(at<void>(ws, L.big_mark), 0, (size_t)p.C * 4, s));
-        CK(cudaMemsetAsync(at<void>(ws, L.cursor), 0, (size_t)p.C * 4, s));
+        // one launch resets the status word, the range starts, the big marks and the cursors
+        k0_init<<<(unsigned)std::max<uint64_t>(1, (std::max<uint64_t>(nranges, p.C) + 255) / 256), 256, 0, s>>>(
+            dst, at<unsigned long long>(ws, L.range_start), nranges, at<uint32_t>(ws, L.big_mark),
+            at<uint32_t>(ws, L.cursor), p.C);
+        CK(cudaGetLastError());
 
         if (chunks && chunks->n > 0) {
             for (int i = 0; i < chunks->n; ++i) {
@@ -918,7 +928,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
             at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
         CK(cudaGetLastError());
         tm.mark();
-        nl.count += (p.local && p.cap1 > 0) ? 6 : 5;
+        nl.count += (p.local && p.cap1 > 0) ? 7 : 6;
 
         CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));

@@ -98,6 +98,9 @@ enum { kPredMufu = 1, kPredMixed = 2, kPredPacked = 3, kPredSkip = 4 };
 // Host emulation (IEEE fma semantics, scripts/k9_pipes.cu notes): max |r2 d - 1| = 6.2e-8
 // (~1 ulp) and r2 is non-increasing in d over every f32 of [1, 2) (the bit trick is
 // scale-invariant, so that binade covers all of them).
+#ifndef MLSORT_RCP_NEWTON2
+#define MLSORT_RCP_NEWTON2 0     // 1: Newton instead of the cubic second step (A/B experiments)
+#endif
 typedef unsigned long long f32x2;
 __device__ __forceinline__ f32x2 pk2(float a, float b) {
     f32x2 r;
@@ -147,7 +150,11 @@ __device__ __forceinline__ f32x2 neg_rcp_packed(f32x2 d2, f32x2 k1_2, f32x2 one2
     f32x2 nr2 = pk2(__uint_as_float(kSeedNeg - __float_as_uint(d0)), __uint_as_float(kSeedNeg - __float_as_uint(d1)));
     nr2 = fmul2(nr2, ffma2(d2, nr2, k1_2));                 // -r1 = -r0 (k1 - d r0)
     const f32x2 e2 = ffma2(d2, nr2, one2);                  // e = 1 - d r1
+#if MLSORT_RCP_NEWTON2
+    return ffma2(nr2, e2, nr2);                             // -r1 (1 + e): |rel| <= 1.7e-6
+#else
     return ffma2(nr2, ffma2(e2, e2, e2), nr2);              // -r1 (1 + e + e^2)
+#endif
 }
 
 // Fixed-point accumulation of Eq. 3: every term w2_j * sigma_j is scaled
