@@ -12,7 +12,10 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libmlsort.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["mlsort.cu", "host_weights.cpp", "host_train.cpp", "comm.cpp"]
+# (source, object suffix, extra flags): mlsort.cu is compiled once per translation-unit slice
+# (-DMLSORT_TU=k, see the split in mlsort.cu) so the slices build in parallel
+SOURCES = [("mlsort.cu", f"tu{k}", [f"-DMLSORT_TU={k}"]) for k in range(5)] + \
+          [("host_weights.cpp", "", []), ("host_train.cpp", "", []), ("comm.cpp", "", [])]
 # NCCL headers (torch-bundled); the library is dlopen-ed at run time (csrc/comm.cpp)
 NCCL_INC = os.environ.get("MLSORT_NCCL_INC", os.path.join(os.path.dirname(sys.executable), "..", "lib",
                           "python%d.%d" % sys.version_info[:2], "site-packages", "nvidia", "nccl", "include"))
@@ -39,11 +42,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objs = []
     procs = []
-    for src in SOURCES:
-        obj = os.path.join(CSRC, "build", src + ".o")
+    for src, suffix, extra in SOURCES:
+        obj = os.path.join(CSRC, "build", src + (("." + suffix) if suffix else "") + ".o")
         os.makedirs(os.path.dirname(obj), exist_ok=True)
         if src.endswith(".cu"):
-            cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
                    "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
             cmd += os.environ.get("MLSORT_NVCC_FLAGS", "").split()     # experiments only (-D...)
             if verbose:

@@ -223,7 +223,7 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
 // region cursors), one CTA.  starts[C] = n.
 // K0: per-call reset of the status word and the per-coarse-bucket bookkeeping (one launch
 // instead of a host copy and three memsets).
-__global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256)
 k0_init(DevStatus* __restrict__ st, unsigned long long* __restrict__ range_start, uint64_t nranges,
         uint32_t* __restrict__ big_mark, uint32_t* __restrict__ cursor, uint32_t C) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -235,7 +235,7 @@ k0_init(DevStatus* __restrict__ st, unsigned long long* __restrict__ range_start
     }
 }
 
-__global__ void __launch_bounds__(1024)
+static __global__ void __launch_bounds__(1024)
 k2_coarse_starts(const uint32_t* __restrict__ cursor, uint32_t C, unsigned long long* __restrict__ starts,
                  bool one_pass) {
     __shared__ uint32_t scratch[64];

@@ -132,7 +132,7 @@ k_radix_hist(const Bits* __restrict__ keys, const uint32_t* __restrict__ vals, u
 // entries and records each tile's total, k_radix_scan (one CTA) scans the tile totals, and
 // k_scan_add adds every tile's offset.
 constexpr int kScanTile = 16384;
-__global__ void __launch_bounds__(1024) k_scan_blocks(uint32_t* __restrict__ a, uint64_t m, uint32_t* __restrict__ tot) {
+static __global__ void __launch_bounds__(1024) k_scan_blocks(uint32_t* __restrict__ a, uint64_t m, uint32_t* __restrict__ tot) {
     __shared__ uint32_t scratch[64];
     const uint64_t t0 = (uint64_t)blockIdx.x * kScanTile;
     const uint64_t s = t0 + threadIdx.x * 16ull;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(1024) k_scan_blocks(uint32_t* __restrict__ a, 
     }
     if (threadIdx.x == 0) tot[blockIdx.x] = total;
 }
-__global__ void k_scan_add(uint32_t* __restrict__ a, uint64_t m, const uint32_t* __restrict__ tot) {
+static __global__ void k_scan_add(uint32_t* __restrict__ a, uint64_t m, const uint32_t* __restrict__ tot) {
     const uint32_t add = tot[blockIdx.x];
     if (!add) return;
     const uint64_t t0 = (uint64_t)blockIdx.x * kScanTile;
@@ -160,7 +160,7 @@ __global__ void k_scan_add(uint32_t* __restrict__ a, uint64_t m, const uint32_t*
 }
 
 // in-place exclusive scan of m entries with one CTA (digit-major order)
-__global__ void __launch_bounds__(1024) k_radix_scan(uint32_t* __restrict__ a, uint64_t m) {
+static __global__ void __launch_bounds__(1024) k_radix_scan(uint32_t* __restrict__ a, uint64_t m) {
     __shared__ uint32_t scratch[64];
     __shared__ uint32_t carry;
     if (threadIdx.x == 0) carry = 0;

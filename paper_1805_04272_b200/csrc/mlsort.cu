@@ -30,6 +30,20 @@
 
 using namespace mlsort;
 
+// Internal helpers live in a namespace named per translation-unit slice (see the split below):
+// the same file is compiled several times, and nvcc gives an anonymous namespace the same
+// external name in every one of those objects.
+#ifndef MLSORT_TU
+#define MLSORT_TU_NAME all
+#else
+#define MLSORT_TU_NAME MLSORT_TU
+#endif
+#define MLSORT_CAT2(a, b) a##b
+#define MLSORT_CAT(a, b) MLSORT_CAT2(a, b)
+#define MLSORT_LOCAL MLSORT_CAT(mlsort_local_tu, MLSORT_TU_NAME)
+namespace MLSORT_LOCAL {}
+using namespace MLSORT_LOCAL;
+
 #define CK(x)                                                                                   \
     do {                                                                                        \
         cudaError_t e_ = (x);                                                                   \
@@ -40,7 +54,7 @@ using namespace mlsort;
         }                                                                                       \
     } while (0)
 
-namespace {
+namespace MLSORT_LOCAL {
 
 constexpr size_t kAlign = 256;
 constexpr double kRegionFactor = 4.0;        // region capacity / average coarse-bucket size
@@ -1070,8 +1084,62 @@ uint64_t workspace_bytes(uint64_t n, mlsort_dtype dt, uint64_t B, bool perm) {
                     make_layout(make_plan(n, B, ks, perm, false)).total);
 }
 
-}  // namespace
+}  // namespace MLSORT_LOCAL
 
+// ==================================================================== translation-unit split
+// run_pipeline<KeyT, PERM, GIVEN> holds almost all kernel instantiations; build.py compiles this
+// file several times with -DMLSORT_TU=k so each variant is instantiated in exactly one object,
+// in parallel (MLSORT_TU = 0: the C ABI and the remaining entry points).  Without MLSORT_TU the
+// file is one self-contained translation unit.
+#ifndef MLSORT_TU
+#define MLSORT_TU (-1)
+#endif
+#define MLSORT_IN_TU(k) (MLSORT_TU == -1 || MLSORT_TU == (k))
+
+#define MLSORT_RUN_ARGS(K)                                                                                     \
+    const K *keys, uint64_t n, uint64_t B, const mlsort::Weights *w, int pred, K *out_keys, uint32_t *out_perm, \
+        void *ws, uint64_t ws_bytes, cudaStream_t s, mlsort_info *info, const uint32_t *bucket_in,            \
+        const uint32_t *idx_in, uint32_t b_lo, bool timing, bool verify_all, const void *chunks
+#define MLSORT_RUN_CALL                                                                                         \
+    keys, n, B, w, pred, out_keys, out_perm, ws, ws_bytes, s, info, bucket_in, idx_in, b_lo, timing, verify_all, \
+        static_cast<const ChunkPlan*>(chunks)
+
+namespace mlsort_tu {
+template <typename KeyT, bool PERM, bool GIVEN>
+int run(MLSORT_RUN_ARGS(KeyT));
+#define MLSORT_RUN_VARIANT(TU, K, P, G)                                                        \
+    template <> int run<K, P, G>(MLSORT_RUN_ARGS(K));
+MLSORT_RUN_VARIANT(1, float, false, false)
+MLSORT_RUN_VARIANT(2, float, true, false)
+MLSORT_RUN_VARIANT(3, double, false, false)
+MLSORT_RUN_VARIANT(3, double, true, false)
+MLSORT_RUN_VARIANT(4, float, false, true)
+MLSORT_RUN_VARIANT(4, float, true, true)
+MLSORT_RUN_VARIANT(4, double, false, true)
+MLSORT_RUN_VARIANT(4, double, true, true)
+#undef MLSORT_RUN_VARIANT
+}  // namespace mlsort_tu
+
+#define MLSORT_RUN_DEFINE(K, P, G)                                                              \
+    template <> int mlsort_tu::run<K, P, G>(MLSORT_RUN_ARGS(K)) { return run_pipeline<K, P, G>(MLSORT_RUN_CALL); }
+#if MLSORT_IN_TU(1)
+MLSORT_RUN_DEFINE(float, false, false)
+#endif
+#if MLSORT_IN_TU(2)
+MLSORT_RUN_DEFINE(float, true, false)
+#endif
+#if MLSORT_IN_TU(3)
+MLSORT_RUN_DEFINE(double, false, false)
+MLSORT_RUN_DEFINE(double, true, false)
+#endif
+#if MLSORT_IN_TU(4)
+MLSORT_RUN_DEFINE(float, false, true)
+MLSORT_RUN_DEFINE(float, true, true)
+MLSORT_RUN_DEFINE(double, false, true)
+MLSORT_RUN_DEFINE(double, true, true)
+#endif
+
+#if MLSORT_IN_TU(0)
 // ==================================================================== C ABI
 
 extern "C" int mlsort_sort_workspace_size(uint64_t n, mlsort_dtype dt, const mlsort_opts* o, int want_perm,
@@ -1087,7 +1155,7 @@ extern "C" int mlsort_sort_workspace_size(uint64_t n, mlsort_dtype dt, const mls
     return MLSORT_OK;
 }
 
-namespace {
+namespace MLSORT_LOCAL {
 int sort_impl(const void* d_keys, const uint32_t* d_payload, uint64_t n, mlsort_dtype dt, const mlsort_weights* wh,
               const mlsort_opts* o, void* d_out_keys, uint32_t* d_out_perm, uint32_t* d_out_payload, void* d_ws,
               uint64_t ws_bytes, void* stream, mlsort_info* info, const ChunkPlan* chunks) {
@@ -1118,14 +1186,14 @@ int sort_impl(const void* d_keys, const uint32_t* d_payload, uint64_t n, mlsort_
     const bool verify_all = o && o->verify == 2;
     int rc;
     if (dt == MLSORT_F32) {
-        rc = perm ? run_pipeline<float, true, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, d_out_perm,
+        rc = perm ? mlsort_tu::run<float, true, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, d_out_perm,
                                                      ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all, chunks)
-                  : run_pipeline<float, false, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, nullptr,
+                  : mlsort_tu::run<float, false, false>((const float*)d_keys, n, B, w, pred, (float*)d_out_keys, nullptr,
                                                       ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all, chunks);
     } else {
-        rc = perm ? run_pipeline<double, true, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
+        rc = perm ? mlsort_tu::run<double, true, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
                                                       d_out_perm, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all, chunks)
-                  : run_pipeline<double, false, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
+                  : mlsort_tu::run<double, false, false>((const double*)d_keys, n, B, w, pred, (double*)d_out_keys,
                                                        nullptr, ws, ws_bytes, s, info, nullptr, nullptr, 0, timing, verify_all, chunks);
     }
     if (rc == MLSORT_OK && d_out_payload) {
@@ -1136,7 +1204,7 @@ int sort_impl(const void* d_keys, const uint32_t* d_payload, uint64_t n, mlsort_
     }
     return rc;
 }
-}  // namespace
+}  // namespace MLSORT_LOCAL
 
 extern "C" int mlsort_sort(const void* d_keys, const uint32_t* d_payload, uint64_t n, mlsort_dtype dt,
                            const mlsort_weights* wh, const mlsort_opts* o, void* d_out_keys, uint32_t* d_out_perm,
@@ -1248,7 +1316,7 @@ extern "C" int mlsort_sort_host(const void* h_keys, uint64_t n, mlsort_dtype dt,
 }
 
 // ---------------------------------------------------------------- approximate ranking
-namespace {
+namespace MLSORT_LOCAL {
 // Each warp evaluates 32 x G consecutive keys (lane + 32 q), so on sorted input a warp spans a
 // narrow value range and the skipping variant (SKIP) drops whole saturated pairs, exactly as on
 // k1_ws's value-grouped tiles.  The clamped chain is used throughout: for keys inside the safe
@@ -1318,7 +1386,7 @@ int launch_predict(const KeyT* keys, uint64_t n, const Weights& w, uint64_t B, i
     CK(cudaGetLastError());
     return MLSORT_OK;
 }
-}  // namespace
+}  // namespace MLSORT_LOCAL
 
 extern "C" int mlsort_predict(const void* d_keys, uint64_t n, mlsort_dtype dt, const mlsort_weights* wh,
                               uint64_t num_buckets, int32_t predictor, float* d_y, uint32_t* d_bucket, void* stream) {
@@ -1447,18 +1515,18 @@ extern "C" int mlsort_sort_records(const void* d_keys, const uint32_t* d_bucket,
     const uint64_t B = bucket_hi - bucket_lo;
     const uint32_t blo = (uint32_t)bucket_lo;
     if (dt == MLSORT_F32)
-        return d_index ? run_pipeline<float, true, true>((const float*)d_keys, n, B, nullptr, kPredMixed,
+        return d_index ? mlsort_tu::run<float, true, true>((const float*)d_keys, n, B, nullptr, kPredMixed,
                                                          (float*)d_out_keys, d_out_index, ws, ws_bytes, s, info,
-                                                         d_bucket, d_index, blo)
-                       : run_pipeline<float, false, true>((const float*)d_keys, n, B, nullptr, kPredMixed,
+                                                         d_bucket, d_index, blo, false, false, nullptr)
+                       : mlsort_tu::run<float, false, true>((const float*)d_keys, n, B, nullptr, kPredMixed,
                                                           (float*)d_out_keys, nullptr, ws, ws_bytes, s, info,
-                                                          d_bucket, nullptr, blo);
-    return d_index ? run_pipeline<double, true, true>((const double*)d_keys, n, B, nullptr, kPredMixed,
+                                                          d_bucket, nullptr, blo, false, false, nullptr);
+    return d_index ? mlsort_tu::run<double, true, true>((const double*)d_keys, n, B, nullptr, kPredMixed,
                                                       (double*)d_out_keys, d_out_index, ws, ws_bytes, s, info,
-                                                      d_bucket, d_index, blo)
-                   : run_pipeline<double, false, true>((const double*)d_keys, n, B, nullptr, kPredMixed,
+                                                      d_bucket, d_index, blo, false, false, nullptr)
+                   : mlsort_tu::run<double, false, true>((const double*)d_keys, n, B, nullptr, kPredMixed,
                                                        (double*)d_out_keys, nullptr, ws, ws_bytes, s, info, d_bucket,
-                                                       nullptr, blo);
+                                                       nullptr, blo, false, false, nullptr);
 }
 
 // ---------------------------------------------------------------- K8: primitive sweeps (A14)
@@ -1493,3 +1561,4 @@ extern "C" int mlsort_selftest_monotone(int32_t primitive, uint64_t* descents, u
     }
     return MLSORT_OK;
 }
+#endif  // MLSORT_IN_TU(0)

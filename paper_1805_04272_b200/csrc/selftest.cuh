@@ -61,7 +61,7 @@ __device__ __forceinline__ float sweep_eval(int what, float x, f32x2 k1_2, f32x2
 // one thread per chunk of kSweepChunk consecutive inputs (+ the first input of the next chunk)
 constexpr uint32_t kSweepChunk = 2048;
 
-__global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256)
 k_sweep_monotone(int what, f32x2 k1_2, f32x2 one2, SweepOut* out) {
     const uint64_t total = sweep_count(what);
     const uint64_t nchunks = (total + kSweepChunk - 1) / kSweepChunk;
