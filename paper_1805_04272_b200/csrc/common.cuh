@@ -26,7 +26,24 @@ struct DevStatus {
     unsigned long long mid_count;   // coarse buckets handed from the primary to the secondary K3 pass
     unsigned long long ticket3b;    // ticket of the secondary K3 pass
     unsigned long long k3_violations;   // order violations found inside K3 slices (cluster K3)
-    unsigned long long pad[1];
+    unsigned long long item_count;  // K3 round items emitted by k3_cut
+    unsigned long long seg_count;   // giant runs handed to the host-driven radix pass
+    unsigned long long ticket3c;    // k3_cut ticket
+    unsigned long long ticket3d;    // K3 round-pass ticket
+    unsigned long long item_overflow;   // items / segments that did not fit their lists
+    unsigned long long pad[3];
+};
+
+// A K3 round item: the rank buckets [f_lo, f_hi) of coarse bucket c, cnt keys, sorted into the
+// output range [out, out + cnt).  A segment: an output range [out, out + len) that still needs
+// the stable radix pass (flags bit0: all keys bit-identical).
+struct K3Item {
+    uint32_t c, f_lo, f_hi, cnt;
+    unsigned long long out;
+};
+struct K3Seg {
+    unsigned long long out, len;
+    uint32_t flags, pad;
 };
 
 // ---- start of coarse bucket c's region: c * capc, or the exact padded layout of a retry

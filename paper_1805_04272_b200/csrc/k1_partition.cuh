@@ -207,7 +207,7 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
         const uint32_t b = stage_b[e];
         const uint32_t c = b >> p.fine_bits;
         const int32_t slot = gadj[c] + (int32_t)e;
-        if (rbase || (uint32_t)slot < p.capc) {
+        if ((unsigned long long)(uint32_t)slot < (rbase ? rbase[c + 1] - rbase[c] : (unsigned long long)p.capc)) {
             const size_t dst = (rbase ? (size_t)rbase[c] : (size_t)c * p.capc) + (uint32_t)slot;
             reg_keys[dst] = stage_key[e];
             reg_fine[dst] = (uint16_t)(b & fmask);
@@ -225,13 +225,14 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
 // instead of a host copy and three memsets).
 static __global__ void __launch_bounds__(256)
 k0_init(DevStatus* __restrict__ st, unsigned long long* __restrict__ range_start, uint64_t nranges,
-        uint32_t* __restrict__ big_mark, uint32_t* __restrict__ cursor, uint32_t C) {
+        uint32_t* __restrict__ big_mark, uint32_t* __restrict__ cursor, uint32_t C, uint32_t* __restrict__ est) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < sizeof(DevStatus) / 8) reinterpret_cast<unsigned long long*>(st)[i] = i == 0 ? ~0ull : 0ull;
     if (i < nranges) range_start[i] = ~0ull;
     if (i < C) {
         big_mark[i] = 0u;
         cursor[i] = 0u;
+        if (est) est[i] = 0u;
     }
 }
 

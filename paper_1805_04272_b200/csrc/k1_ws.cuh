@@ -331,7 +331,7 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
         // ---- scan (warp rows, conflict-free) + reservation of this tile's piece in every region.
         // gbase[c] = region slot of the tile's staged position 0 for coarse bucket c, so a staged
         // element at position pos goes to gbase[c] + pos.  Regions start at c * capc, or at
-        // rbase[c] (exact, padded sizes: the retry after an overflow).  A piece that would overflow
+        // rbase[c] (sampled sizes, K0, or exact ones: the retry after an overflow).  A piece that would overflow
         // its region is marked kOverflowBase and not stored; the call then retries with exact
         // regions from the final cursors.
         {
@@ -352,7 +352,10 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
                 const uint32_t ex = carry + x - v;             // exclusive within the warp's chunk
                 if (c < b1) {
                     hist[c] = ex;
-                    const bool fits = rbase != nullptr || (unsigned long long)g + v <= p.capc;
+                    // region capacity: capc (fixed layout) or rbase[c+1] - rbase[c] (sampled /
+                    // exact layouts, K0 / the retry)
+                    const unsigned long long rcap = rbase ? rbase[c + 1] - rbase[c] : (unsigned long long)p.capc;
+                    const bool fits = (unsigned long long)g + v <= rcap;
                     over |= !fits;
                     const long long rb = rbase ? (long long)rbase[c] : (long long)c * p.capc;
                     gbase[c] = fits ? rb + (long long)g - (long long)ex : kOverflowBase;

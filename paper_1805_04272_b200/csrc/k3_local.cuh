@@ -25,6 +25,7 @@
 #include <algorithm>
 
 #include "k3_sort.cuh"
+#include "k3_big.cuh"
 
 namespace mlsort {
 
@@ -61,6 +62,7 @@ struct K3LParams {
     uint32_t secondary;     // 0: pass over all coarse buckets; 1: pass over mid_list
     uint32_t to_mid;        // too-large buckets go to mid_list (1, primary of two passes) or to
                             // K4's big_list (0)
+    uint32_t item_cap;      // ITEMS pass: capacity of the item list (k3_big.cuh)
 };
 
 // The rank-bucket histogram holds two u16 counters per 32-bit word (a coarse bucket never
@@ -331,14 +333,18 @@ __device__ __forceinline__ bool k3l_store_verify(const typename KeyTraits<KeyT>:
     return bad;
 }
 
-template <typename KeyT, bool PERM, int NT>
+// ITEMS = true: the round pass over the items of k3_cut (k3_big.cuh): work item t sorts the rank
+// buckets [f_lo, f_hi) of coarse bucket c -- it reads c's whole region and keeps only those --
+// into the output range starting at `out`; everything else is the same code.
+template <typename KeyT, bool PERM, int NT, bool ITEMS = false>
 __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
 k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __restrict__ reg_fine,
               const uint32_t* __restrict__ reg_idx, const unsigned long long* __restrict__ starts,
               KeyT* __restrict__ out_keys, uint32_t* __restrict__ out_perm,
               unsigned long long* __restrict__ range_start, DevStatus* __restrict__ st,
               uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_mark, uint32_t* __restrict__ mid_list,
-              unsigned long long* __restrict__ ticket, const unsigned long long* __restrict__ rbase) {
+              unsigned long long* __restrict__ ticket, const unsigned long long* __restrict__ rbase,
+              const K3Item* __restrict__ item_list = nullptr) {
     using Bits = typename KeyTraits<KeyT>::Bits;
     extern __shared__ __align__(16) unsigned char smem[];
     // ctrl words: [1] next ticket, [2] big-queue count, [8..72) scan scratch,
@@ -352,18 +358,19 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
     uint32_t* sidx = reinterpret_cast<uint32_t*>(skey + p.cap);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // work items: coarse ids 0..C-1 (primary) or mid_list[0..mid_count) (secondary)
-    const uint32_t items = p.secondary ? (uint32_t)st->mid_count : p.num_coarse;
-    auto coarse_of = [&](uint32_t t) { return p.secondary ? mid_list[t] : t; };
-    const uint32_t hw = (p.kfine + 1u) / 2u;           // histogram words
-    const uint32_t hwp = k3l_hist_words(p.kfine);      // padded to a multiple of 4
+    // work items: coarse ids 0..C-1 (primary), mid_list[0..mid_count) (secondary) or the
+    // k3_cut items (ITEMS)
+    const uint32_t items = ITEMS ? (uint32_t)min(st->item_count, (unsigned long long)p.item_cap)
+                                 : (p.secondary ? (uint32_t)st->mid_count : p.num_coarse);
+    auto coarse_of = [&](uint32_t t) { return ITEMS ? item_list[t].c : (p.secondary ? mid_list[t] : t); };
     if (tid == 0) {
         const uint32_t t0 = (uint32_t)atomicAdd(ticket, 1ull);
         ctrl[1] = t0;
         if (t0 < items) {
             const uint32_t c0 = coarse_of(t0);
             const unsigned long long s0 = starts[c0], n0 = starts[c0 + 1] - s0;
-            if (n0 <= p.cap) prefetch_bucket<KeyT, PERM>(reg_keys, reg_fine, reg_idx, region_base(rbase, c0, p.capc), n0);
+            if (ITEMS || n0 <= p.cap)
+                prefetch_bucket<KeyT, PERM>(reg_keys, reg_fine, reg_idx, region_base(rbase, c0, p.capc), n0);
         }
     }
 #ifdef MLSORT_K3L_TIMING
@@ -375,9 +382,24 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         K3L_T(0);
         const uint32_t t = ctrl[1];
         if (t >= items) break;
-        const uint32_t c = coarse_of(t);
-        const unsigned long long S0 = starts[c];
-        const uint32_t n = (uint32_t)min(starts[c + 1] - S0, (unsigned long long)0xffffffffull);
+        uint32_t c, n, nreg, f_lo = 0u, kf = p.kfine;
+        unsigned long long S0;
+        if (ITEMS) {
+            const K3Item it = item_list[t];
+            c = it.c;
+            S0 = it.out;
+            n = it.cnt;                        // keys of this item
+            f_lo = it.f_lo;
+            kf = it.f_hi - it.f_lo;            // its rank buckets
+            nreg = (uint32_t)(starts[c + 1] - starts[c]);   // keys in c's region (all read)
+        } else {
+            c = coarse_of(t);
+            S0 = starts[c];
+            n = (uint32_t)min(starts[c + 1] - S0, (unsigned long long)0xffffffffull);
+            nreg = n;
+        }
+        const uint32_t hw = (kf + 1u) / 2u;            // histogram words
+        const uint32_t hwp = k3l_hist_words(kf);       // padded to a multiple of 4
         __syncthreads();                       // everyone read ctrl[1]
         if (tid == 0) {                        // take the next bucket now and prefetch it into L2
             const uint32_t t1 = (uint32_t)atomicAdd(ticket, 1ull);
@@ -387,7 +409,8 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             if (t1 < items) {
                 const uint32_t c1 = coarse_of(t1);
                 const unsigned long long s1 = starts[c1], n1 = starts[c1 + 1] - s1;
-                if (n1 <= p.cap) prefetch_bucket<KeyT, PERM>(reg_keys, reg_fine, reg_idx, region_base(rbase, c1, p.capc), n1);
+                if (ITEMS || n1 <= p.cap)
+                    prefetch_bucket<KeyT, PERM>(reg_keys, reg_fine, reg_idx, region_base(rbase, c1, p.capc), n1);
             }
 #endif
         }
@@ -404,11 +427,15 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         };
         if (n == 0) {
             prefetch_next();
-            if (tid == 0) range_start[c] = ~0ull;
+            if (!ITEMS && tid == 0) range_start[c] = ~0ull;
             continue;
         }
         if (n > p.cap) {                       // too large for this pass
             prefetch_next();
+            if (ITEMS) {                       // (k3_cut never emits one)
+                if (tid == 0) atomicAdd(&st->item_overflow, 1ull);
+                continue;
+            }
             if (tid == 0) {
                 atomicMax(&st->max_coarse, (unsigned long long)n);
                 if (p.to_mid) {
@@ -421,7 +448,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             }
             continue;
         }
-        if (tid == 0) {
+        if (!ITEMS && tid == 0) {
             range_start[c] = S0;
             atomicMax(&st->max_coarse, (unsigned long long)n);
         }
@@ -429,8 +456,23 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         const KeyT* gk = reg_keys + rb;
         const uint16_t* gf = reg_fine + rb;
         const uint32_t* gi = PERM ? reg_idx + rb : nullptr;
-        const uint32_t n8 = n >> 3;
+        const uint32_t n8 = nreg >> 3;
         const uint4* g8 = reinterpret_cast<const uint4*>(gf);
+        // rank bucket of a region element inside this work item (ITEMS: f - f_lo, else f);
+        // >= kf means "not in this item" (unsigned compare)
+        auto rel = [&](uint32_t f) { return ITEMS ? f - f_lo : f; };
+        auto hinc8 = [&](const uint4 v) {
+            if (!ITEMS) {
+                hist_add8(h2, v);
+            } else {
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t f = rel((w4[k >> 1] >> (16 * (k & 1))) & 0xffffu);
+                    if (f < kf) hist_inc(h2, f);
+                }
+            }
+        };
 
         // ---- 1. histogram of rank buckets (8 ids per 128-bit load; rows are 16-B aligned)
         for (uint32_t w = tid; w < hwp; w += NT) h2[w] = 0u;
@@ -445,9 +487,12 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         }
 #pragma unroll
         for (int k = 0; k < kL3FineRegs; ++k)
-            if (tid + k * NT < n8) hist_add8(h2, fr[k]);
-        for (uint32_t i = tid + kL3FineRegs * NT; i < n8; i += NT) hist_add8(h2, __ldg(g8 + i));
-        for (uint32_t q = (n8 << 3) + tid; q < n; q += NT) hist_inc(h2, gf[q]);
+            if (tid + k * NT < n8) hinc8(fr[k]);
+        for (uint32_t i = tid + kL3FineRegs * NT; i < n8; i += NT) hinc8(__ldg(g8 + i));
+        for (uint32_t q = (n8 << 3) + tid; q < nreg; q += NT) {
+            const uint32_t f = rel(gf[q]);
+            if (!ITEMS || f < kf) hist_inc(h2, f);
+        }
         __syncthreads();
         K3L_T(1);
         // ---- 2. exclusive scan of the counters: thread t scans its own WPT consecutive words
@@ -515,7 +560,8 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             const uint32_t fw[4] = {fv.x, fv.y, fv.z, fv.w};
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const uint32_t f = (fw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+                const uint32_t f = rel((fw[k >> 1] >> (16 * (k & 1))) & 0xffffu);
+                if (ITEMS && f >= kf) continue;
                 const uint32_t pos = hist_inc_ret(h2, f);
                 skey[pos] = KeyTraits<KeyT>::to_ord(kv[k]);
                 if (PERM) sidx[pos] = iv[k];
@@ -525,8 +571,9 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         for (int k = 0; k < kL3FineRegs; ++k)
             if (tid + k * NT < n8) place8(tid + k * NT, fr[k]);
         for (uint32_t i = tid + kL3FineRegs * NT; i < n8; i += NT) place8(i, __ldg(g8 + i));
-        for (uint32_t q = (n8 << 3) + tid; q < n; q += NT) {
-            const uint32_t f = gf[q];
+        for (uint32_t q = (n8 << 3) + tid; q < nreg; q += NT) {
+            const uint32_t f = rel(gf[q]);
+            if (ITEMS && f >= kf) continue;
             const uint32_t pos = hist_inc_ret(h2, f);
             skey[pos] = KeyTraits<KeyT>::to_ord(gk[q]);
             if (PERM) sidx[pos] = gi[q];

@@ -27,6 +27,7 @@
 #include "k4_overflow.cuh"
 #include "dist.cuh"
 #include "selftest.cuh"
+#include "k0_sample.cuh"
 
 using namespace mlsort;
 
@@ -327,7 +328,27 @@ struct Plan {
     bool ws = false;         // K1 = warp-specialized persistent k1_ws (tile = ws tile), else k1_predict_partition
     bool ws_group = false;   // k1_ws with value grouping + saturated-pair skipping
     uint32_t kfine = 0;      // rank buckets per coarse bucket (local plan)
+    uint32_t item_cap = 0;   // local plan: k3_cut item list / segment list capacities (k3_big.cuh)
+    uint32_t seg_cap = 0;
+    bool sampled = false;    // regions sized from a sample of the predicted buckets (K0)
+    uint64_t stride = 1;     // K0: every stride-th key is predicted
+    uint64_t area = 0;       // region slots (all coarse buckets)
 };
+
+// Regions sized by K0 (k0_sample.cuh) for inputs large enough that fixed 4x regions waste GBs
+// and skewed data overflows them (one more K1 pass); small inputs keep the fixed layout.
+constexpr uint64_t kSampledMinN = 1ull << 27;
+constexpr uint64_t kSampleTarget = 1ull << 22;     // sampled keys per call
+
+void set_region_area(Plan& p) {
+    if (p.sampled) {
+        const double S = (double)p.stride, C = (double)p.C, n = (double)p.n;
+        p.area = (uint64_t)(n + 6.0 * std::sqrt(S * C * (n + S * C)) + 72.0 * C) + 64;
+        p.area = (p.area + 7) & ~7ull;
+    } else {
+        p.area = (uint64_t)p.C * p.capc;
+    }
+}
 
 size_t k3_elem_bytes(size_t ks, bool perm) { return ks * 2 + 4 + (perm ? 8 : 0); }
 
@@ -343,6 +364,10 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
 // its shared memory fits (and the caller predicts), else the phase-alternating one.
 Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws = true, bool group = false) {
     Plan p = make_plan_base(n, B, ks, perm, allow_ws);
+    // K0-sized regions: predicting sorts only (the records path has no network to sample)
+    p.sampled = allow_ws && n >= kSampledMinN && !std::getenv("MLSORT_NO_SAMPLE");
+    p.stride = std::max<uint64_t>(1, n / kSampleTarget);
+    set_region_area(p);
     if (allow_ws) {
         const uint32_t wt = ws_tile_of(ks, group);
         const size_t sm = k1ws_smem_bytes(ks, wt, p.C, group);
@@ -357,6 +382,14 @@ Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws = tru
     return p;
 }
 
+// k3_cut emits at most 2 n_c / (cap/2) + 2 items per coarse bucket plus one empty item per giant
+// rank bucket, and at most n / cap + 1 segments per ... (k3_big.cuh): bounded by the totals
+void set_item_caps(Plan& p) {
+    const uint64_t cap = std::max<uint32_t>(p.cap, 2);
+    p.item_cap = (uint32_t)std::min<uint64_t>(0x7FFFFFFFull, 8 * p.n / cap + 4ull * p.C + 64);
+    p.seg_cap = (uint32_t)std::min<uint64_t>(0x7FFFFFFFull, 2 * p.n / cap + p.C + 64);
+}
+
 Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws) {
     Plan p;
     p.n = n;
@@ -365,7 +398,6 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
     p.perm = perm;
     p.tile = kTileSmall;
     p.T = (uint32_t)((n + p.tile - 1) / p.tile);
-    const size_t eb = k3_elem_bytes(ks, perm);
     const uint32_t lb = ceil_log2(B);
     const uint32_t fb_max = std::min<uint32_t>(16, lb);
     const uint32_t fb_min = lb > 14 ? lb - 14 : 0;   // C <= 16384
@@ -400,57 +432,38 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
         uint64_t cc = (uint64_t)std::ceil(kRegionFactor * avg) + 64;
         cc = (cc + 7) & ~7ull;
         p.capc = (uint32_t)std::min<uint64_t>(cc, 0xFFFFFFF0ull);
+        set_item_caps(p);
         return p;
     }
-    bool found = false;
-    for (int fb = (int)fb_max; fb >= (int)fb_min && !found; --fb) {
+    // No rank-bucket split gives an average coarse bucket that one CTA holds with margin (large
+    // f64 inputs, a CTA's shared memory being the limit): the most coarse buckets K1 allows,
+    // and k3_cut splits every coarse bucket that does not fit into items that do (k3_big.cuh).
+    for (int fb = (int)std::max(fb_min, 0u); fb <= (int)fb_max; ++fb) {
         const uint64_t C = (B + (1ull << fb) - 1) >> fb;
-        const size_t k1 = k1_smem_bytes(ks, perm, p.tile, (uint32_t)C);
-        if (k1 > 227 * 1024) continue;
-        const double avg = (double)n * (double)(1ull << fb) / (double)B;
-        for (uint32_t R = 1; R <= 8; R <<= 1) {
-            if ((1u << fb) < R) break;
-            const uint32_t kr = (1u << fb) / R;
-            if (kr > 16384) continue;
-            const long long capll = ((long long)kK3SmemBudget - kCtrlBytes - 16 - 4ll * kr) / (long long)eb;
-            if (capll < 64) continue;
-            if (avg <= 0.5 * R * (double)capll) {
-                p.fb = (uint32_t)fb;
-                p.C = (uint32_t)C;
-                p.R = R;
-                p.kr = kr;
-                p.cap = (uint32_t)capll;
-                p.k1_smem = k1;
-                found = true;
-                break;
-            }
-        }
-    }
-    if (!found) {   // heavily skewed sizes: smallest coarse buckets K1 allows, overflow path does the rest
-        uint32_t fbc = std::min<uint32_t>(fb_max, 16);
-        for (int fb = (int)std::max(fb_min, 0u); fb <= (int)std::min<uint32_t>(fb_max, 16); ++fb) {
-            const uint64_t C = (B + (1ull << fb) - 1) >> fb;
-            const bool k1_ok = k1_smem_bytes(ks, perm, p.tile, (uint32_t)C) <= kK1SmemMax ||
-                               (allow_ws && k1ws_smem_bytes(ks, ws_tile_of(ks), (uint32_t)C) <= kK1WsSmemMax);
-            if (k1_ok) {
-                fbc = (uint32_t)fb;
-                break;
-            }
-        }
-        p.fb = fbc;
-        p.C = (uint32_t)((B + (1ull << p.fb) - 1) >> p.fb);
-        p.R = (1u << p.fb) >= 8 ? 8 : (1u << p.fb);
-        p.kr = (1u << p.fb) / p.R;
-        p.cap = (uint32_t)(((long long)kK3SmemBudget - kCtrlBytes - 16 - 4ll * p.kr) / (long long)eb);
+        const bool k1_ok = k1_smem_bytes(ks, perm, p.tile, (uint32_t)C) <= kK1SmemMax ||
+                           (allow_ws && k1ws_smem_bytes(ks, ws_tile_of(ks), (uint32_t)C) <= kK1WsSmemMax);
+        if (!k1_ok && fb < (int)fb_max) continue;
+        const uint32_t kfine = 1u << fb;
+        p.local = true;
+        p.fb = (uint32_t)fb;
+        p.C = (uint32_t)C;
+        p.R = 1;
+        p.kr = kfine;
+        p.kfine = kfine;
+        p.cap = k3l_cap_for(kK3LSmemMax, ks, perm, kfine, kL3ThreadsBig);
         p.k1_smem = k1_smem_bytes(ks, perm, p.tile, p.C);
+        p.k3_smem = k3l_smem_bytes(ks, perm, kfine, p.cap, kL3ThreadsBig);
+        p.cap1 = 0;
+        p.k3_smem1 = 0;
+        break;
     }
+    set_item_caps(p);
     {   // region capacity: kRegionFactor x the average coarse bucket, multiple of 8 (16 B rows)
         const double avg = (double)n * (double)(1ull << p.fb) / (double)B;
         uint64_t cc = (uint64_t)std::ceil(kRegionFactor * avg) + 64;
         cc = (cc + 7) & ~7ull;
         p.capc = (uint32_t)std::min<uint64_t>(cc, 0xFFFFFFF0ull);
     }
-    p.k3_smem = kCtrlBytes + (size_t)p.cap * ks * 2 + (size_t)p.kr * 4 + (perm ? (size_t)p.cap * 8 : 0) + (size_t)p.cap * 4 + 16;
     return p;
 }
 
@@ -458,7 +471,7 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
 struct Layout {
     size_t status = 0, reg_keys = 0, reg_fine = 0, reg_idx = 0, cursor = 0, starts = 0,
            range_start = 0, big_list = 0, flags = 0, big_mark = 0, radix = 0, mid_list = 0, segs = 0, rbase = 0,
-           total = 0;
+           items = 0, k3segs = 0, est = 0, total = 0;
     size_t radix_bytes = 0;
 };
 
@@ -479,7 +492,7 @@ Layout make_layout(const Plan& p) {
     L.status = take(sizeof(DevStatus));
     // regions (K1 -> K3/K4) and the radix area (K4 radix / fallback) are never live together
     // C regions of capc slots, plus one tile of trash rows for pieces that overflow a region
-    const uint64_t slots = (uint64_t)p.C * p.capc + p.tile;
+    const uint64_t slots = p.area + p.tile;
     const size_t reg_bytes = align_up(slots * p.ks) + align_up(slots * 2) + (p.perm ? align_up(slots * 4) : 0);
     const size_t rad = radix_area(p.n, p.ks, p.perm);
     const size_t shared_area = std::max(reg_bytes, rad);
@@ -496,8 +509,11 @@ Layout make_layout(const Plan& p) {
     L.flags = take((size_t)p.C * 4);
     L.big_mark = take((size_t)p.C * 4);
     L.mid_list = take((size_t)p.C * 4);
-    L.segs = take((size_t)p.C * 24);
-    L.rbase = take((size_t)p.C * 8);
+    L.segs = take((size_t)std::max<uint32_t>(p.C, p.seg_cap) * 24);
+    L.rbase = take((size_t)(p.C + 1) * 8);
+    L.items = take((size_t)p.item_cap * sizeof(K3Item));
+    L.k3segs = take((size_t)p.seg_cap * sizeof(K3Seg));
+    L.est = take((size_t)p.C * 4);
     L.total = off;
     return L;
 }
@@ -638,11 +654,11 @@ cudaError_t launch_k3_t(const Plan& p, void* ws, const Layout& L, KeyT* out_keys
                               at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.big_mark), rbase);
 }
 
-template <typename KeyT, bool PERM, int NT>
+template <typename KeyT, bool PERM, int NT, bool ITEMS = false>
 cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s,
                            bool secondary, bool to_mid, uint32_t cap, size_t smem, int grid,
                            const unsigned long long* rbase) {
-    auto kern = k3_local_sort<KeyT, PERM, NT>;
+    auto kern = k3_local_sort<KeyT, PERM, NT, ITEMS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     K3LParams kp;
@@ -652,13 +668,44 @@ cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_k
     kp.cap = cap;
     kp.secondary = secondary ? 1u : 0u;
     kp.to_mid = to_mid ? 1u : 0u;
+    kp.item_cap = p.item_cap;
     DevStatus* st = at<DevStatus>(ws, L.status);
+    unsigned long long* ticket = ITEMS ? &st->ticket3d : (secondary ? &st->ticket3b : &st->ticket3);
     kern<<<grid, NT, smem, s>>>(kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
                                 PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr, at<unsigned long long>(ws, L.starts),
                                 out_keys, out_perm, at<unsigned long long>(ws, L.range_start), st,
                                 at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.big_mark), at<uint32_t>(ws, L.mid_list),
-                                secondary ? &st->ticket3b : &st->ticket3, rbase);
+                                ticket, rbase, at<K3Item>(ws, L.items));
     return cudaGetLastError();
+}
+
+// Coarse buckets too large for the K3 passes: k3_cut splits them into items (and copies giant
+// rank buckets to their output ranges), then the round pass sorts the items (k3_big.cuh).
+template <typename KeyT, bool PERM>
+cudaError_t launch_k3_big(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm,
+                          cudaStream_t s, const unsigned long long* rbase) {
+    auto cut = k3_cut<KeyT, PERM>;
+    uint32_t gshift = 0;
+    while ((p.kfine >> gshift) > kCutGroups) ++gshift;
+    const size_t smem = (size_t)(2 * (p.kfine >> gshift) + 2) * 4;
+    cudaError_t e = cudaFuncSetAttribute(cut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    K3CutParams cp;
+    cp.capc = p.capc;
+    cp.kfine = p.kfine;
+    cp.cap = p.cap;
+    cp.item_cap = p.item_cap;
+    cp.seg_cap = p.seg_cap;
+    cp.gshift = gshift;
+    cut<<<std::min<int>(num_sms(), (int)p.C), kCutThreads, smem, s>>>(
+        cp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine), PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
+        at<unsigned long long>(ws, L.starts), at<uint32_t>(ws, L.big_list), at<DevStatus>(ws, L.status),
+        at<K3Item>(ws, L.items), at<K3Seg>(ws, L.k3segs), out_keys, out_perm, at<unsigned long long>(ws, L.range_start),
+        rbase);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_k3_pass<KeyT, PERM, kL3ThreadsBig, true>(p, ws, L, out_keys, out_perm, s, false, false, p.cap,
+                                                            p.k3_smem, num_sms(), rbase);
 }
 
 // K3 local plan: primary pass (two 512-thread CTAs per SM, capacity cap1) over every coarse
@@ -672,11 +719,14 @@ cudaError_t launch_k3_local(const Plan& p, void* ws, const Layout& L, KeyT* out_
         e = launch_k3_pass<KeyT, PERM, kL3Threads>(p, ws, L, out_keys, out_perm, s, false, true, p.cap1,
                                                    p.k3_smem1, std::min<int>(2 * num_sms(), (int)p.C), rbase);
         if (e != cudaSuccess) return e;
-        return launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, true, false,
-                                                         p.cap, p.k3_smem, num_sms(), rbase);
+        e = launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, true, false,
+                                                      p.cap, p.k3_smem, num_sms(), rbase);
+    } else {
+        e = launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, false, false,
+                                                      p.cap, p.k3_smem, std::min<int>(num_sms(), (int)p.C), rbase);
     }
-    return launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, false, false,
-                                                     p.cap, p.k3_smem, std::min<int>(num_sms(), (int)p.C), rbase);
+    if (e != cudaSuccess) return e;
+    return launch_k3_big<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase);
 }
 
 template <typename KeyT, bool PERM>
@@ -868,6 +918,28 @@ struct PhaseTimer {
     }
 };
 
+template <typename KeyT>
+cudaError_t launch_k0(const Plan& p, const KeyT* keys, uint32_t mpad, const FoldedWeights& fw, const K1Params& kp,
+                      void* ws, const Layout& L, cudaStream_t s) {
+    const size_t smem = (size_t)p.C * 4;
+    const uint64_t ns = (p.n + p.stride - 1) / p.stride;
+    const int grid = (int)std::min<uint64_t>((uint64_t)num_sms() * 2, (ns + 2047) / 2048 + 1);
+    cudaError_t e = cudaSuccess;
+#define K0CASE(M)                                                                                          \
+    if (mpad == M) {                                                                                       \
+        e = cudaFuncSetAttribute(k0_sample<KeyT, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                    \
+        k0_sample<KeyT, M><<<grid, 256, smem, s>>>(keys, p.n, p.stride, fw, kp, at<uint32_t>(ws, L.est));  \
+    }
+    K0CASE(16) K0CASE(32) K0CASE(64)
+#undef K0CASE
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k0_regions<<<1, 1024, 0, s>>>(at<uint32_t>(ws, L.est), p.C, p.stride, (unsigned long long)p.area,
+                                  at<unsigned long long>(ws, L.rbase));
+    return cudaGetLastError();
+}
+
 template <typename KeyT, bool PERM, bool GIVEN>
 int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int pred, KeyT* out_keys,
                  uint32_t* out_perm, void* ws, uint64_t ws_bytes, cudaStream_t s, mlsort_info* info,
@@ -900,14 +972,21 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     DevStatus* dst = at<DevStatus>(ws, L.status);
     DevStatus* hs = host_status();
     DevStatus st;
-    const unsigned long long* rbase = nullptr;   // regions at c * capc; exact layout on a retry
+    const unsigned long long* rbase = nullptr;   // regions at c * capc; K0-sized or exact (retry) layouts
     const uint64_t nranges = (uint64_t)p.C * p.R;
     for (int attempt = 0;; ++attempt) {
         // one launch resets the status word, the range starts, the big marks and the cursors
         k0_init<<<(unsigned)std::max<uint64_t>(1, (std::max<uint64_t>(nranges, p.C) + 255) / 256), 256, 0, s>>>(
             dst, at<unsigned long long>(ws, L.range_start), nranges, at<uint32_t>(ws, L.big_mark),
-            at<uint32_t>(ws, L.cursor), p.C);
+            at<uint32_t>(ws, L.cursor), p.C, (p.sampled && attempt == 0) ? at<uint32_t>(ws, L.est) : nullptr);
         CK(cudaGetLastError());
+        if (!GIVEN && p.sampled && attempt == 0) {        // K0: regions from a sample of the buckets
+            if (chunks)                                   // (the sample spans every chunk)
+                for (int i = 0; i < chunks->n; ++i) CK(cudaStreamWaitEvent(s, chunks->ready[i], 0));
+            CK((launch_k0<KeyT>(p, keys, mpad, fw, kp, ws, L, s)));
+            rbase = at<unsigned long long>(ws, L.rbase);
+            nl.count += 2;
+        }
 
         if (chunks && chunks->n > 0) {
             for (int i = 0; i < chunks->n; ++i) {
@@ -932,17 +1011,24 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         // model, fused with its store; K5 checks every coarse-bucket boundary.
         CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase)));
         tm.mark();
-        k4_big_copy<KeyT, PERM><<<num_sms(), kK3Threads, 0, s>>>(
-            p.capc, p.R, at<KeyT>(ws, L.reg_keys), PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
-            at<unsigned long long>(ws, L.starts), out_keys, out_perm, at<unsigned long long>(ws, L.range_start), dst,
-            at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.flags), &dst->ticket, rbase);
-        CK(cudaGetLastError());
+        if (!p.local) {       // cluster plans: K4 copies the overflow buckets (local plans: k3_cut)
+            k4_big_copy<KeyT, PERM><<<num_sms(), kK3Threads, 0, s>>>(
+                p.capc, p.R, at<KeyT>(ws, L.reg_keys), PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
+                at<unsigned long long>(ws, L.starts), out_keys, out_perm, at<unsigned long long>(ws, L.range_start),
+                dst, at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.flags), &dst->ticket, rbase);
+            CK(cudaGetLastError());
+        }
         tm.mark();
         k5_boundary_verify<KeyT, PERM><<<(unsigned)((nranges + 255) / 256), 256, 0, s>>>(
             at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
         CK(cudaGetLastError());
+        if (p.local) {
+            k5_item_verify<KeyT, PERM><<<num_sms() * 2, 256, 0, s>>>(at<K3Item>(ws, L.items), at<K3Seg>(ws, L.k3segs),
+                                                                     out_keys, out_perm, dst, p.item_cap, p.seg_cap, n);
+            CK(cudaGetLastError());
+        }
         tm.mark();
-        nl.count += (p.local && p.cap1 > 0) ? 7 : 6;
+        nl.count += p.local ? 7 + (p.cap1 > 0 ? 1 : 0) : 6;
 
         CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -960,15 +1046,16 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         if (st.region_overflow > 0 && attempt == 0 && st.bad_index == ~0ull) {
             std::vector<uint32_t> sizes(p.C);
             CK(cudaMemcpy(sizes.data(), at<uint32_t>(ws, L.cursor), (size_t)p.C * 4, cudaMemcpyDeviceToHost));
-            std::vector<unsigned long long> rb(p.C);
+            std::vector<unsigned long long> rb(p.C + 1);
             unsigned long long off = 0;
             for (uint32_t c = 0; c < p.C; ++c) {
                 rb[c] = off;
                 off += ((unsigned long long)sizes[c] + 7ull) & ~7ull;
             }
-            if (off <= (unsigned long long)p.C * p.capc) {
+            rb[p.C] = off;
+            if (off <= p.area) {
                 unsigned long long* d_rb = at<unsigned long long>(ws, L.rbase);
-                CK(cudaMemcpyAsync(d_rb, rb.data(), (size_t)p.C * 8, cudaMemcpyHostToDevice, s));
+                CK(cudaMemcpyAsync(d_rb, rb.data(), (size_t)(p.C + 1) * 8, cudaMemcpyHostToDevice, s));
                 rbase = d_rb;
                 continue;
             }
@@ -983,30 +1070,46 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     // K5 boundary violations plus violations found inside cluster-K3 slices
     uint64_t violations = st.violations + st.k3_violations;
     if (st.region_overflow > 0) violations += 1;   // a region was full: use the conventional sort
-    if (st.region_overflow == 0 && st.overflow > 0) {   // K4 radix for big buckets that are not all-equal
-        std::vector<uint32_t> big(st.big_count), flags(st.big_count);
-        std::vector<unsigned long long> starts(p.C + 1);
-        CK(cudaMemcpyAsync(big.data(), at<uint32_t>(ws, L.big_list), big.size() * 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(flags.data(), at<uint32_t>(ws, L.flags), flags.size() * 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(starts.data(), at<unsigned long long>(ws, L.starts), starts.size() * 8,
-                           cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        // one radix sort over the union of the overflow buckets that still need sorting
+    if (st.item_overflow > 0) violations += 1;     // (lists sized for the worst case: not expected)
+    const bool need_radix = st.region_overflow == 0 && (p.local ? st.seg_count > 0 : st.overflow > 0);
+    if (need_radix) {   // the stable radix pass over the runs K3 / K4 could not sort
         std::vector<unsigned long long> seg;
         uint64_t tot = 0;
         bool all_equal = true;
-        std::vector<uint32_t> order(big.size());
-        for (size_t k = 0; k < big.size(); ++k) order[k] = (uint32_t)k;
-        std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return big[a] < big[b]; });
-        for (uint32_t k : order) {
-            const bool equal = flags[k] & 1u;
-            if (equal && !PERM) continue;
-            all_equal &= equal;
-            const uint64_t S0 = starts[big[k]], len = starts[big[k] + 1] - S0;
-            seg.push_back(S0);
-            seg.push_back(tot);
-            seg.push_back(len);
-            tot += len;
+        if (p.local) {
+            const uint64_t nseg_dev = std::min<uint64_t>(st.seg_count, p.seg_cap);
+            std::vector<K3Seg> ks(nseg_dev);
+            CK(cudaMemcpyAsync(ks.data(), at<K3Seg>(ws, L.k3segs), nseg_dev * sizeof(K3Seg), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            std::sort(ks.begin(), ks.end(), [](const K3Seg& a, const K3Seg& b) { return a.out < b.out; });
+            for (const K3Seg& g : ks) {
+                all_equal &= (g.flags & 1u) != 0;
+                seg.push_back(g.out);
+                seg.push_back(tot);
+                seg.push_back(g.len);
+                tot += g.len;
+            }
+        } else {
+            std::vector<uint32_t> big(st.big_count), flags(st.big_count);
+            std::vector<unsigned long long> starts(p.C + 1);
+            CK(cudaMemcpyAsync(big.data(), at<uint32_t>(ws, L.big_list), big.size() * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(flags.data(), at<uint32_t>(ws, L.flags), flags.size() * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(starts.data(), at<unsigned long long>(ws, L.starts), starts.size() * 8,
+                               cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            std::vector<uint32_t> order(big.size());
+            for (size_t k = 0; k < big.size(); ++k) order[k] = (uint32_t)k;
+            std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return big[a] < big[b]; });
+            for (uint32_t k : order) {
+                const bool equal = flags[k] & 1u;
+                if (equal && !PERM) continue;
+                all_equal &= equal;
+                const uint64_t S0 = starts[big[k]], len = starts[big[k] + 1] - S0;
+                seg.push_back(S0);
+                seg.push_back(tot);
+                seg.push_back(len);
+                tot += len;
+            }
         }
         if (tot > 0) {
             using Bits = typename KeyTraits<KeyT>::Bits;
@@ -1036,11 +1139,15 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         CK(cudaMemsetAsync(&dst->violations, 0, 8, s));
         k5_boundary_verify<KeyT, PERM><<<(unsigned)((nranges + 255) / 256), 256, 0, s>>>(
             at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
+        if (p.local)
+            k5_item_verify<KeyT, PERM><<<num_sms() * 2, 256, 0, s>>>(at<K3Item>(ws, L.items), at<K3Seg>(ws, L.k3segs),
+                                                                     out_keys, out_perm, dst, p.item_cap, p.seg_cap, n);
         CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         // the first K5 pass ran before the overflow buckets were sorted: only the fresh boundary
         // check counts, together with the slice-internal K3 violations
-        violations = st.k3_violations + hs->violations + (st.region_overflow > 0 ? 1 : 0);
+        violations = st.k3_violations + hs->violations + (st.region_overflow > 0 ? 1 : 0) +
+                     (st.item_overflow > 0 ? 1 : 0);
     }
     if (std::getenv("MLSORT_DEBUG"))
         fprintf(stderr, "mlsort: plan C=%u fb=%u R=%u local=%d ws=%d group=%d cap=%u cap1=%u | k5=%llu k3=%llu "
