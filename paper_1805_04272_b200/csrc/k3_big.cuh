@@ -61,6 +61,9 @@ k3_cut(K3CutParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __restr
     const uint32_t T = max(1u, p.cap / 2), heavy = p.cap - T;
     const uint32_t per = (K + kCutThreads - 1) / kCutThreads;       // rank buckets per thread
     const uint32_t f0 = min(K, (uint32_t)tid * per), f1 = min(K, f0 + per);
+    // a region overflowed in K1: the regions are incomplete (the call re-runs with an exact
+    // layout), and a region's count may exceed what it holds -- read nothing
+    if (st->region_overflow) return;
     while (true) {
         if (tid == 0) s_t = (uint32_t)atomicAdd(&st->ticket3c, 1ull);
         __syncthreads();

@@ -358,6 +358,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
     uint32_t* sidx = reinterpret_cast<uint32_t*>(skey + p.cap);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (st->region_overflow) return;       // K1 overflowed a region: incomplete regions, re-run follows
     // work items: coarse ids 0..C-1 (primary), mid_list[0..mid_count) (secondary) or the
     // k3_cut items (ITEMS)
     const uint32_t items = ITEMS ? (uint32_t)min(st->item_count, (unsigned long long)p.item_cap)

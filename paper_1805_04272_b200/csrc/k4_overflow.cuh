@@ -1,74 +1,21 @@
-// k4_overflow.cuh -- K4 overflow path, K5 boundary verify, and the conventional-sort
-// fallback (a stable LSD radix sort).
+// k4_overflow.cuh -- K5 boundary verify, and the stable LSD radix sort that finishes what the
+// rank buckets cannot.
 //
-// The paper sorts the keys that its model cannot place well with "conventional sorting
-// algorithms (like Quick Sort)" (§3 l.121, tails) and SPEC escalates to a full
-// comparison sort when verification fails.  Here a coarse bucket too large
-// for K3's distributed shared memory (heavy duplicates, e.g. BASELINE C5, or a skewed
-// model) is first gathered in tile order with each tile's piece sorted by input index, so
-// the gathered run is in input order; an all-equal run is then already final (stable
-// copy-through), otherwise a stable LSD radix sort by key finishes it.  The same radix
-// sort, applied to the whole input, is the fallback when the verify pass finds a
-// violation (non-monotone weights, reading A14).
+// The paper sorts the keys its model cannot place well with "conventional sorting algorithms
+// (like Quick Sort)" (§3 l.121, tails), and SPEC escalates to a full comparison sort
+// when verification fails.  Here the radix sort (8-bit digits, stable,
+// digit-major chunk histograms, smem-staged coalesced scatter) sorts (a) the SEGMENTS k3_cut
+// hands over -- a single rank bucket larger than a CTA whose keys differ, or an all-equal run
+// of a permutation sort, which only needs its input indices ordered (k3_big.cuh) -- gathered
+// into one array, sorted once and scattered back (valid because the monotone network orders
+// the segments), and (b) the whole input when a verify pass finds a violation (a non-monotone
+// model, reading A14).
 #pragma once
 
 #include "common.cuh"
 #include "k3_sort.cuh"
 
 namespace mlsort {
-
-// ------------------------------------------------------------------ K4 copy-out
-// Persistent CTAs take big coarse buckets from big_list, copy the bucket's region (K1 left it
-// contiguous) to the bucket's output range and test whether all keys are equal.
-// flags[k] bit0: all keys bit-identical (a key-only run is then final; a perm run only needs
-// its indices sorted).
-template <typename KeyT, bool PERM>
-__global__ void __launch_bounds__(kK3Threads)
-k4_big_copy(uint32_t capc, uint32_t R, const KeyT* __restrict__ reg_keys, const uint32_t* __restrict__ reg_idx,
-            const unsigned long long* __restrict__ starts, KeyT* __restrict__ out_keys,
-            uint32_t* __restrict__ out_perm, unsigned long long* __restrict__ range_start,
-            DevStatus* __restrict__ st, const uint32_t* __restrict__ big_list, uint32_t* __restrict__ flags,
-            unsigned long long* __restrict__ ticket, const unsigned long long* __restrict__ rbase) {
-    using Bits = typename KeyTraits<KeyT>::Bits;
-    __shared__ uint32_t s_k;
-    __shared__ unsigned long long s_min, s_max;
-    const int tid = threadIdx.x;
-    const unsigned long long nbig = st->big_count;
-    while (true) {
-        if (tid == 0) {
-            s_k = (uint32_t)atomicAdd(ticket, 1ull);
-            s_min = ~0ull;
-            s_max = 0ull;
-        }
-        __syncthreads();
-        const uint32_t k = s_k;
-        if (k >= nbig) return;
-        const uint32_t c = big_list[k];
-        const unsigned long long S0 = starts[c], n_c = starts[c + 1] - S0;
-        if (tid == 0) range_start[(size_t)c * R] = S0;
-        const size_t rb0 = region_base(rbase, c, capc);
-        Bits vmin = ~(Bits)0, vmax = 0;
-        for (unsigned long long i = tid; i < n_c; i += kK3Threads) {
-            const KeyT key = reg_keys[rb0 + i];
-            const Bits ob = KeyTraits<KeyT>::to_ord(key);
-            vmin = ob < vmin ? ob : vmin;
-            vmax = ob > vmax ? ob : vmax;
-            out_keys[S0 + i] = key;
-            if (PERM) out_perm[S0 + i] = reg_idx[rb0 + i];
-        }
-        if (vmin != ~(Bits)0) {
-            atomicMin(&s_min, (unsigned long long)vmin);
-            atomicMax(&s_max, (unsigned long long)vmax);
-        }
-        __syncthreads();
-        if (tid == 0) {
-            const bool equal = (s_min == s_max);
-            flags[k] = equal ? 1u : 0u;
-            if (!equal || PERM) atomicAdd(&st->overflow, 1ull);   // needs the K4 radix pass
-        }
-        __syncthreads();
-    }
-}
 
 // ------------------------------------------------------------------ K5 boundary verify
 // Every K3 slice / K4 run recorded its output start; check the pair that straddles it.
@@ -122,7 +69,10 @@ k_radix_hist(const Bits* __restrict__ keys, const uint32_t* __restrict__ vals, u
     const uint64_t base = (uint64_t)blockIdx.x * kRadixChunk;
     for (int k = 0; k < kRadixItems; ++k) {
         const uint64_t e = base + threadIdx.x + (uint64_t)k * kRadixThreads;
-        if (e < n) atomicAdd(&h[radix_digit<Bits>(keys[e], vals ? vals[e] : 0u, field, shift)], 1u);
+        if (e < n) {   // read only the array the digit comes from
+            const uint32_t d = field == 0 ? (uint32_t)((keys[e] >> shift) & 255u) : ((vals[e] >> shift) & 255u);
+            atomicAdd(&h[d], 1u);
+        }
     }
     __syncthreads();
     for (int d = threadIdx.x; d < 256; d += kRadixThreads) ghist[(size_t)d * nchunks + blockIdx.x] = h[d];
@@ -184,6 +134,10 @@ static __global__ void __launch_bounds__(1024) k_radix_scan(uint32_t* __restrict
 }
 
 // Stable scatter: warp w owns elements [w*512, (w+1)*512) of the chunk, processed in lane order.
+// Every element's rank among the chunk's elements of its digit is computed first; the chunk is
+// then laid out in digit order in shared memory and written out position by position, so the
+// consecutive threads of a warp store consecutive addresses of one digit's run (coalesced)
+// instead of 32 scattered 4-byte stores per warp instruction.
 template <typename Bits>
 __global__ void __launch_bounds__(kRadixThreads)
 k_radix_scatter(const Bits* __restrict__ kin, const uint32_t* __restrict__ vin, Bits* __restrict__ kout,
@@ -191,12 +145,17 @@ k_radix_scatter(const Bits* __restrict__ kin, const uint32_t* __restrict__ vin, 
                 const uint32_t* __restrict__ ghist) {
     constexpr int W = kRadixThreads / 32;
     __shared__ uint16_t wcnt[W][256];
-    __shared__ uint32_t goff[256];
+    __shared__ uint32_t goff[256], loff[257];
+    extern __shared__ __align__(16) unsigned char rsm[];     // chunk in digit order (dynamic)
+    Bits* sk = reinterpret_cast<Bits*>(rsm);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(sk + kRadixChunk);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < W * 256; i += kRadixThreads) (&wcnt[0][0])[i] = 0;
     for (int d = threadIdx.x; d < 256; d += kRadixThreads) goff[d] = ghist[(size_t)d * nchunks + blockIdx.x];
     __syncthreads();
-    const uint64_t base = (uint64_t)blockIdx.x * kRadixChunk + (uint64_t)warp * 32 * kRadixItems;
+    const uint64_t cbase = (uint64_t)blockIdx.x * kRadixChunk;
+    const uint32_t cnt = (uint32_t)min((uint64_t)kRadixChunk, n - cbase);
+    const uint64_t base = cbase + (uint64_t)warp * 32 * kRadixItems;
     Bits k[kRadixItems];
     uint32_t v[kRadixItems], rank[kRadixItems], dig[kRadixItems];
     const unsigned lt = (1u << lane) - 1u;
@@ -215,26 +174,62 @@ k_radix_scatter(const Bits* __restrict__ kin, const uint32_t* __restrict__ vin, 
         __syncwarp();
     }
     __syncthreads();
-    // exclusive prefix over warps for each digit
-    for (int d = threadIdx.x; d < 256; d += kRadixThreads) {
+    // exclusive prefix over warps for each digit, and the chunk-local start of each digit
+    if (threadIdx.x < 256) {
+        const int d = threadIdx.x;
         uint32_t run = 0;
         for (int w = 0; w < W; ++w) {
             const uint32_t c = wcnt[w][d];
             wcnt[w][d] = (uint16_t)run;
             run += c;
         }
+        loff[d] = run;                                // digit total (scanned below)
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {                           // exclusive scan of the 256 digit totals
+        uint32_t t[8], sum = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            t[i] = loff[threadIdx.x * 8 + i];
+            sum += t[i];
+        }
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        uint32_t run = x - sum;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            loff[threadIdx.x * 8 + i] = run;
+            run += t[i];
+        }
+        if (threadIdx.x == 31) loff[256] = run;
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kRadixItems; ++r) {
         const uint64_t e = base + (uint64_t)r * 32 + lane;
         if (e < n) {
-            const uint64_t dst = (uint64_t)goff[dig[r]] + wcnt[warp][dig[r]] + rank[r];
-            kout[dst] = k[r];
-            if (vout) vout[dst] = v[r];
+            const uint32_t lp = loff[dig[r]] + wcnt[warp][dig[r]] + rank[r];
+            sk[lp] = k[r];
+            if (vout) sv[lp] = v[r];
         }
     }
+    __syncthreads();
+    for (uint32_t lp = threadIdx.x; lp < cnt; lp += kRadixThreads) {
+        const Bits kk = sk[lp];
+        const uint32_t vv = vout ? sv[lp] : 0u;
+        const uint32_t d = radix_digit<Bits>(kk, vv, field, shift);
+        const uint64_t dst = (uint64_t)goff[d] + (lp - loff[d]);
+        kout[dst] = kk;
+        if (vout) vout[dst] = vv;
+    }
 }
+
+template <typename Bits>
+constexpr size_t radix_scatter_smem() { return (size_t)kRadixChunk * (sizeof(Bits) + 4); }
 
 // ------------------------------------------------------------------ batched overflow sort
 // The overflow buckets are sorted together: their ranges are gathered into one contiguous
@@ -264,6 +259,28 @@ __global__ void k_seg_scatter(const unsigned long long* __restrict__ seg, uint32
             keys[src + i] = KeyTraits<KeyT>::from_ord(tk[dst + i]);
             if (tv) perm[src + i] = tv[dst + i];
         }
+    }
+}
+
+// all-equal runs: the radix key is the run's ordinal g (runs are gathered in output order), the
+// value the input index; only the indices are scattered back
+template <typename Bits>
+__global__ void k_seg_gather_ordinal(const unsigned long long* __restrict__ seg, uint32_t nseg,
+                                     const uint32_t* __restrict__ perm, Bits* __restrict__ tk,
+                                     uint32_t* __restrict__ tv) {
+    for (uint32_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+        const unsigned long long src = seg[3 * g], dst = seg[3 * g + 1], len = seg[3 * g + 2];
+        for (unsigned long long i = threadIdx.x; i < len; i += blockDim.x) {
+            tk[dst + i] = (Bits)g;
+            tv[dst + i] = perm[src + i];
+        }
+    }
+}
+static __global__ void k_seg_scatter_perm(const unsigned long long* __restrict__ seg, uint32_t nseg,
+                                          const uint32_t* __restrict__ tv, uint32_t* __restrict__ perm) {
+    for (uint32_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+        const unsigned long long src = seg[3 * g], dst = seg[3 * g + 1], len = seg[3 * g + 2];
+        for (unsigned long long i = threadIdx.x; i < len; i += blockDim.x) perm[src + i] = tv[dst + i];
     }
 }
 

@@ -620,40 +620,6 @@ cudaError_t launch_k1(const Plan& p, const KeyT* keys, uint32_t mpad, int pred, 
     return cudaErrorInvalidValue;
 }
 
-template <typename KeyT, bool PERM, int R>
-cudaError_t launch_k3_t(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm,
-                        cudaStream_t s, const unsigned long long* rbase) {
-    auto kern = k3_cluster_sort<KeyT, PERM, R>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k3_smem);
-    if (e != cudaSuccess) return e;
-    K3Params kp;
-    kp.capc = p.capc;
-    kp.num_coarse = p.C;
-    kp.owner_shift = p.fb - ceil_log2(p.R);
-    kp.kr = p.kr;
-    kp.cap = p.cap;
-    kp.pad = 0;
-    cudaLaunchConfig_t cfg;
-    std::memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3(p.C * R);
-    cfg.blockDim = dim3(kK3Threads);
-    cfg.dynamicSmemBytes = p.k3_smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = R;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, kp, (const KeyT*)at<KeyT>(ws, L.reg_keys),
-                              (const uint16_t*)at<uint16_t>(ws, L.reg_fine),
-                              (const uint32_t*)(PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr),
-                              (const unsigned long long*)at<unsigned long long>(ws, L.starts), out_keys, out_perm,
-                              at<unsigned long long>(ws, L.range_start), at<DevStatus>(ws, L.status),
-                              at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.big_mark), rbase);
-}
-
 template <typename KeyT, bool PERM, int NT, bool ITEMS = false>
 cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s,
                            bool secondary, bool to_mid, uint32_t cap, size_t smem, int grid,
@@ -703,9 +669,18 @@ cudaError_t launch_k3_big(const Plan& p, void* ws, const Layout& L, KeyT* out_ke
         at<K3Item>(ws, L.items), at<K3Seg>(ws, L.k3segs), out_keys, out_perm, at<unsigned long long>(ws, L.range_start),
         rbase);
     e = cudaGetLastError();
+    if (std::getenv("MLSORT_SYNC_DEBUG")) {
+        e = cudaStreamSynchronize(s);
+        fprintf(stderr, "mlsort: k3_cut -> %s\n", cudaGetErrorString(e));
+    }
     if (e != cudaSuccess) return e;
-    return launch_k3_pass<KeyT, PERM, kL3ThreadsBig, true>(p, ws, L, out_keys, out_perm, s, false, false, p.cap,
-                                                            p.k3_smem, num_sms(), rbase);
+    e = launch_k3_pass<KeyT, PERM, kL3ThreadsBig, true>(p, ws, L, out_keys, out_perm, s, false, false, p.cap,
+                                                         p.k3_smem, num_sms(), rbase);
+    if (std::getenv("MLSORT_SYNC_DEBUG")) {
+        e = cudaStreamSynchronize(s);
+        fprintf(stderr, "mlsort: k3 rounds -> %s\n", cudaGetErrorString(e));
+    }
+    return e;
 }
 
 // K3 local plan: primary pass (two 512-thread CTAs per SM, capacity cap1) over every coarse
@@ -725,6 +700,10 @@ cudaError_t launch_k3_local(const Plan& p, void* ws, const Layout& L, KeyT* out_
         e = launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, false, false,
                                                       p.cap, p.k3_smem, std::min<int>(num_sms(), (int)p.C), rbase);
     }
+    if (std::getenv("MLSORT_SYNC_DEBUG")) {
+        e = cudaStreamSynchronize(s);
+        fprintf(stderr, "mlsort: k3 passes -> %s\n", cudaGetErrorString(e));
+    }
     if (e != cudaSuccess) return e;
     return launch_k3_big<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase);
 }
@@ -732,15 +711,7 @@ cudaError_t launch_k3_local(const Plan& p, void* ws, const Layout& L, KeyT* out_
 template <typename KeyT, bool PERM>
 cudaError_t launch_k3(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s,
                       const unsigned long long* rbase) {
-    if (p.local) return launch_k3_local<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase);
-    switch (p.R) {
-        case 1: return launch_k3_t<KeyT, PERM, 1>(p, ws, L, out_keys, out_perm, s, rbase);
-        case 2: return launch_k3_t<KeyT, PERM, 2>(p, ws, L, out_keys, out_perm, s, rbase);
-        case 4: return launch_k3_t<KeyT, PERM, 4>(p, ws, L, out_keys, out_perm, s, rbase);
-        case 8: return launch_k3_t<KeyT, PERM, 8>(p, ws, L, out_keys, out_perm, s, rbase);
-        default: break;
-    }
-    return cudaErrorInvalidValue;
+    return launch_k3_local<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase);
 }
 
 // Stable LSD radix sort of (ord bits, payload) pairs, n elements, in the radix area.
@@ -748,9 +719,13 @@ cudaError_t launch_k3(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, 
 // then over the key digits.  Returns the buffer index (0/1) holding the result.
 template <typename Bits>
 int radix_sort_pairs(Bits* k0, uint32_t* v0, Bits* k1, uint32_t* v1, uint32_t* ghist, uint64_t n,
-                     bool payload_first, cudaStream_t s, Launches& nl, cudaError_t& err, bool skip_keys = false) {
+                     bool payload_first, cudaStream_t s, Launches& nl, cudaError_t& err, bool skip_keys = false,
+                     int key_bits = (int)(sizeof(Bits) * 8)) {
     const uint32_t nchunks = (uint32_t)((n + kRadixChunk - 1) / kRadixChunk);
     int cur = 0;
+    err = cudaFuncSetAttribute(k_radix_scatter<Bits>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)radix_scatter_smem<Bits>());
+    if (err != cudaSuccess) return 0;
     auto pass = [&](int field, int shift) {
         Bits* ki = cur ? k1 : k0;
         uint32_t* vi = cur ? v1 : v0;
@@ -770,14 +745,15 @@ int radix_sort_pairs(Bits* k0, uint32_t* v0, Bits* k1, uint32_t* v1, uint32_t* g
                 nl.count += 2;
             }
         }
-        k_radix_scatter<Bits><<<nchunks, kRadixThreads, 0, s>>>(ki, vi, ko, vo, n, field, shift, nchunks, ghist);
+        k_radix_scatter<Bits><<<nchunks, kRadixThreads, radix_scatter_smem<Bits>(), s>>>(ki, vi, ko, vo, n, field, shift,
+                                                                                        nchunks, ghist);
         nl.count += 3;
         cur ^= 1;
     };
     if (payload_first && v0)
         for (int sh = 0; sh < 32; sh += 8) pass(1, sh);
     if (!skip_keys)
-        for (int sh = 0; sh < (int)(sizeof(Bits) * 8); sh += 8) pass(0, sh);
+        for (int sh = 0; sh < key_bits; sh += 8) pass(0, sh);
     err = cudaGetLastError();
     return cur;
 }
@@ -1011,24 +987,15 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         // model, fused with its store; K5 checks every coarse-bucket boundary.
         CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase)));
         tm.mark();
-        if (!p.local) {       // cluster plans: K4 copies the overflow buckets (local plans: k3_cut)
-            k4_big_copy<KeyT, PERM><<<num_sms(), kK3Threads, 0, s>>>(
-                p.capc, p.R, at<KeyT>(ws, L.reg_keys), PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
-                at<unsigned long long>(ws, L.starts), out_keys, out_perm, at<unsigned long long>(ws, L.range_start),
-                dst, at<uint32_t>(ws, L.big_list), at<uint32_t>(ws, L.flags), &dst->ticket, rbase);
-            CK(cudaGetLastError());
-        }
         tm.mark();
         k5_boundary_verify<KeyT, PERM><<<(unsigned)((nranges + 255) / 256), 256, 0, s>>>(
             at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
         CK(cudaGetLastError());
-        if (p.local) {
-            k5_item_verify<KeyT, PERM><<<num_sms() * 2, 256, 0, s>>>(at<K3Item>(ws, L.items), at<K3Seg>(ws, L.k3segs),
-                                                                     out_keys, out_perm, dst, p.item_cap, p.seg_cap, n);
-            CK(cudaGetLastError());
-        }
+        k5_item_verify<KeyT, PERM><<<num_sms() * 2, 256, 0, s>>>(at<K3Item>(ws, L.items), at<K3Seg>(ws, L.k3segs),
+                                                                 out_keys, out_perm, dst, p.item_cap, p.seg_cap, n);
+        CK(cudaGetLastError());
         tm.mark();
-        nl.count += p.local ? 7 + (p.cap1 > 0 ? 1 : 0) : 6;
+        nl.count += 7 + (p.cap1 > 0 ? 1 : 0);
 
         CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1071,45 +1038,22 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     uint64_t violations = st.violations + st.k3_violations;
     if (st.region_overflow > 0) violations += 1;   // a region was full: use the conventional sort
     if (st.item_overflow > 0) violations += 1;     // (lists sized for the worst case: not expected)
-    const bool need_radix = st.region_overflow == 0 && (p.local ? st.seg_count > 0 : st.overflow > 0);
-    if (need_radix) {   // the stable radix pass over the runs K3 / K4 could not sort
+    const bool need_radix = st.region_overflow == 0 && st.seg_count > 0;
+    if (need_radix) {   // the stable radix pass over the runs K3 could not sort (k3_cut segments)
         std::vector<unsigned long long> seg;
         uint64_t tot = 0;
         bool all_equal = true;
-        if (p.local) {
-            const uint64_t nseg_dev = std::min<uint64_t>(st.seg_count, p.seg_cap);
-            std::vector<K3Seg> ks(nseg_dev);
-            CK(cudaMemcpyAsync(ks.data(), at<K3Seg>(ws, L.k3segs), nseg_dev * sizeof(K3Seg), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            std::sort(ks.begin(), ks.end(), [](const K3Seg& a, const K3Seg& b) { return a.out < b.out; });
-            for (const K3Seg& g : ks) {
-                all_equal &= (g.flags & 1u) != 0;
-                seg.push_back(g.out);
-                seg.push_back(tot);
-                seg.push_back(g.len);
-                tot += g.len;
-            }
-        } else {
-            std::vector<uint32_t> big(st.big_count), flags(st.big_count);
-            std::vector<unsigned long long> starts(p.C + 1);
-            CK(cudaMemcpyAsync(big.data(), at<uint32_t>(ws, L.big_list), big.size() * 4, cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(flags.data(), at<uint32_t>(ws, L.flags), flags.size() * 4, cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(starts.data(), at<unsigned long long>(ws, L.starts), starts.size() * 8,
-                               cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            std::vector<uint32_t> order(big.size());
-            for (size_t k = 0; k < big.size(); ++k) order[k] = (uint32_t)k;
-            std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return big[a] < big[b]; });
-            for (uint32_t k : order) {
-                const bool equal = flags[k] & 1u;
-                if (equal && !PERM) continue;
-                all_equal &= equal;
-                const uint64_t S0 = starts[big[k]], len = starts[big[k] + 1] - S0;
-                seg.push_back(S0);
-                seg.push_back(tot);
-                seg.push_back(len);
-                tot += len;
-            }
+        const uint64_t nseg_dev = std::min<uint64_t>(st.seg_count, p.seg_cap);
+        std::vector<K3Seg> ks(nseg_dev);
+        CK(cudaMemcpyAsync(ks.data(), at<K3Seg>(ws, L.k3segs), nseg_dev * sizeof(K3Seg), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::sort(ks.begin(), ks.end(), [](const K3Seg& a, const K3Seg& b) { return a.out < b.out; });
+        for (const K3Seg& g : ks) {
+            all_equal &= (g.flags & 1u) != 0;
+            seg.push_back(g.out);
+            seg.push_back(tot);
+            seg.push_back(g.len);
+            tot += g.len;
         }
         if (tot > 0) {
             using Bits = typename KeyTraits<KeyT>::Bits;
@@ -1123,15 +1067,25 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
             uint32_t* v1 = PERM ? reinterpret_cast<uint32_t*>(rbase + 2 * align_up(tot * sizeof(Bits)) + align_up(tot * 4)) : nullptr;
             uint32_t* gh = reinterpret_cast<uint32_t*>(rbase + 2 * align_up(tot * sizeof(Bits)) + (PERM ? 2 * align_up(tot * 4) : 0));
             const int sg = (int)std::min<uint32_t>(nseg, (uint32_t)num_sms() * 8);
-            k_seg_gather<KeyT><<<sg, 256, 0, s>>>(d_seg, nseg, out_keys, out_perm, k0, v0);
             cudaError_t err;
-            // all-equal perm buckets only need their indices ordered, but buckets hold different
-            // keys, so the key digits are still sorted unless every bucket is all-equal and there
-            // is only one of them
-            const bool skip_keys = all_equal && nseg == 1;
-            int cur = radix_sort_pairs<Bits>(k0, v0, k1, v1, gh, tot, PERM, s, nl, err, skip_keys);
-            if (err != cudaSuccess) return MLSORT_ERR_CUDA;
-            k_seg_scatter<KeyT><<<sg, 256, 0, s>>>(d_seg, nseg, cur ? k1 : k0, cur ? v1 : v0, out_keys, out_perm);
+            if (PERM && all_equal && nseg > 1) {
+                // every run is all-equal: only the indices inside each run need ordering, so the
+                // radix key is the run's ordinal (its keys are already in place) -- 4 index passes
+                // plus ceil(log2(runs)/8) ordinal passes instead of 4 + 8*sizeof(key) / 8
+                k_seg_gather_ordinal<Bits><<<sg, 256, 0, s>>>(d_seg, nseg, out_perm, k0, v0);
+                int bits = 0;
+                while ((1ull << bits) < nseg) ++bits;
+                int cur = radix_sort_pairs<Bits>(k0, v0, k1, v1, gh, tot, true, s, nl, err, false, bits);
+                if (err != cudaSuccess) return MLSORT_ERR_CUDA;
+                k_seg_scatter_perm<<<sg, 256, 0, s>>>(d_seg, nseg, cur ? v1 : v0, out_perm);
+            } else {
+                k_seg_gather<KeyT><<<sg, 256, 0, s>>>(d_seg, nseg, out_keys, out_perm, k0, v0);
+                // a single all-equal perm run only needs its indices ordered
+                const bool skip_keys = all_equal && nseg == 1;
+                int cur = radix_sort_pairs<Bits>(k0, v0, k1, v1, gh, tot, PERM, s, nl, err, skip_keys);
+                if (err != cudaSuccess) return MLSORT_ERR_CUDA;
+                k_seg_scatter<KeyT><<<sg, 256, 0, s>>>(d_seg, nseg, cur ? k1 : k0, cur ? v1 : v0, out_keys, out_perm);
+            }
             CK(cudaGetLastError());
             nl.count += 2;
         }
@@ -1139,9 +1093,8 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         CK(cudaMemsetAsync(&dst->violations, 0, 8, s));
         k5_boundary_verify<KeyT, PERM><<<(unsigned)((nranges + 255) / 256), 256, 0, s>>>(
             at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
-        if (p.local)
-            k5_item_verify<KeyT, PERM><<<num_sms() * 2, 256, 0, s>>>(at<K3Item>(ws, L.items), at<K3Seg>(ws, L.k3segs),
-                                                                     out_keys, out_perm, dst, p.item_cap, p.seg_cap, n);
+        k5_item_verify<KeyT, PERM><<<num_sms() * 2, 256, 0, s>>>(at<K3Item>(ws, L.items), at<K3Seg>(ws, L.k3segs),
+                                                                 out_keys, out_perm, dst, p.item_cap, p.seg_cap, n);
         CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         // the first K5 pass ran before the overflow buckets were sorted: only the fresh boundary
