@@ -39,7 +39,7 @@ struct K1Params {
     // sparse evaluation"), so the clamp changes no output bit; inside them no logistic argument
     // exceeds 120, so the predictor needs no per-activation clamp (FoldedWeights::u_safe_*).
     float u_cl_lo, u_cl_hi;
-    uint32_t pad0;
+    uint32_t flags;          // k1_ws: kK1StageKeys = keys staged in shared memory for the piece stores
 };
 
 template <typename KeyT> __device__ __forceinline__ void key_to_u(KeyT x, const K1Params& p, float& uh, float& ul);

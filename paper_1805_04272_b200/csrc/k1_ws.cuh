@@ -50,14 +50,17 @@ __host__ __device__ constexpr int ws_tile(bool group = false) {
 }
 inline int ws_threads(bool group) { return group ? WsCfg<float, true>::kThreads : WsCfg<float, false>::kThreads; }
 
-// smem: sb[2][T] u32 | stage_key[T] KeyT | hist[C'] u32 | gbase[C'] i64 | stage_e[T] u16 |
+// smem: sb[2][T] u32 | stage_key[T] KeyT (staged plans) | hist[C'] u32 | gbase[C'] i64 | stage_e[T] u16 |
 //       (GROUP: cls_u[T] f32 | cls_e[T] u16 | chist[64] | ccur[64] | lut[2048] u8) | scratch
-// (C' = C rounded up to a multiple of 4 so every array stays 16-B aligned)
+// (C' = C rounded up to a multiple of 4 so every array stays 16-B aligned).  Without key staging
+// (K1Params::flags bit0 clear: plans whose C does not leave room for it) the piece stores
+// re-read each key from the tile in global memory (L2-resident) instead of shared memory.
 __host__ __device__ inline uint32_t k1ws_c2(uint32_t num_coarse) { return (num_coarse + 3u) & ~3u; }
-inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse, bool group = false) {
-    return (size_t)tile * 8 + (size_t)tile * ks + (size_t)k1ws_c2(num_coarse) * 12 + (size_t)tile * 2 +
+inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse, bool group = false, bool stage = true) {
+    return (size_t)tile * 8 + (stage ? (size_t)tile * ks : 0) + (size_t)k1ws_c2(num_coarse) * 12 + (size_t)tile * 2 +
            (group ? (size_t)tile * 6 + kClasses * 8 + 2048 : 0) + 256;
 }
+constexpr uint32_t kK1StageKeys = 1u;      // K1Params::flags
 constexpr long long kOverflowBase = LLONG_MIN;   // gbase marker of a piece that overflowed its region
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -85,8 +88,9 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
     enum { kFull0 = 1, kEmpty0 = 3, kPart = 5, kPred = 6 };
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* sb = reinterpret_cast<uint32_t*>(smem);                         // [2][T]
+    const bool staged = (p.flags & kK1StageKeys) != 0;
     KeyT* stage_key = reinterpret_cast<KeyT*>(smem + (size_t)T * 8);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (size_t)T * 8 + (size_t)T * sizeof(KeyT));
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (size_t)T * 8 + (staged ? (size_t)T * sizeof(KeyT) : 0));
     const uint32_t C = p.num_coarse;
     long long* gbase = reinterpret_cast<long long*>(hist + k1ws_c2(C));   // region slot of staged position 0
     uint16_t* stage_e = reinterpret_cast<uint16_t*>(gbase + k1ws_c2(C));
@@ -378,7 +382,7 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
         for (uint32_t e = pt; e < cnt; e += kPartThreads) {
             const uint32_t pos = atomicAdd(&hist[sbb[e] >> fbits], 1u);
             stage_e[pos] = (uint16_t)e;
-            stage_key[pos] = keys[base + e];                   // L2-resident re-read
+            if (staged) stage_key[pos] = keys[base + e];       // L2-resident re-read
         }
         nbar_sync(kPart, kPartThreads);
         // ---- store every piece into its coarse bucket's region
@@ -389,7 +393,7 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
             const long long gb = gbase[b >> fbits];
             if (gb != kOverflowBase) {
                 const size_t dst = (size_t)(gb + (long long)pos);
-                reg_keys[dst] = stage_key[pos];
+                reg_keys[dst] = staged ? stage_key[pos] : keys[base + e];
                 reg_fine[dst] = (uint16_t)(b & fmask);
                 if (PERM) reg_idx[dst] = (uint32_t)(base + e);
             }

@@ -326,6 +326,7 @@ struct Plan {
     uint32_t cap1 = 0;       // local plan: primary-pass capacity (two CTAs per SM)
     size_t k3_smem1 = 0;     // local plan: primary-pass shared memory
     bool ws = false;         // K1 = warp-specialized persistent k1_ws (tile = ws tile), else k1_predict_partition
+    bool ws_stage = true;    // k1_ws stages the keys in shared memory (else re-reads them from L2)
     bool ws_group = false;   // k1_ws with value grouping + saturated-pair skipping
     uint32_t kfine = 0;      // rank buckets per coarse bucket (local plan)
     uint32_t item_cap = 0;   // local plan: k3_cut item list / segment list capacities (k3_big.cuh)
@@ -370,7 +371,9 @@ Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws = tru
     set_region_area(p);
     if (allow_ws) {
         const uint32_t wt = ws_tile_of(ks, group);
-        const size_t sm = k1ws_smem_bytes(ks, wt, p.C, group);
+        size_t sm = k1ws_smem_bytes(ks, wt, p.C, group, true);
+        p.ws_stage = sm <= kK1WsSmemMax && !std::getenv("MLSORT_NO_STAGE");
+        if (!p.ws_stage) sm = k1ws_smem_bytes(ks, wt, p.C, group, false);
         if (sm <= kK1WsSmemMax) {
             p.ws = true;
             p.ws_group = group;
@@ -410,7 +413,7 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
         if (fb_force >= 0 && fb != fb_force) continue;
         const uint64_t C = (B + (1ull << fb) - 1) >> fb;
         const size_t k1 = k1_smem_bytes(ks, perm, p.tile, (uint32_t)C);
-        const bool ws_fits = allow_ws && k1ws_smem_bytes(ks, ws_tile_of(ks), (uint32_t)C) <= kK1WsSmemMax;
+        const bool ws_fits = allow_ws && k1ws_smem_bytes(ks, ws_tile_of(ks), (uint32_t)C, false, false) <= kK1WsSmemMax;
         if (k1 > kK1SmemMax && !ws_fits) continue;
         const uint32_t kfine = 1u << fb;
         const uint64_t cap = k3l_cap_for(kK3LSmemMax, ks, perm, kfine, kL3ThreadsBig);
@@ -441,7 +444,7 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
     for (int fb = (int)std::max(fb_min, 0u); fb <= (int)fb_max; ++fb) {
         const uint64_t C = (B + (1ull << fb) - 1) >> fb;
         const bool k1_ok = k1_smem_bytes(ks, perm, p.tile, (uint32_t)C) <= kK1SmemMax ||
-                           (allow_ws && k1ws_smem_bytes(ks, ws_tile_of(ks), (uint32_t)C) <= kK1WsSmemMax);
+                           (allow_ws && k1ws_smem_bytes(ks, ws_tile_of(ks), (uint32_t)C, false, false) <= kK1WsSmemMax);
         if (!k1_ok && fb < (int)fb_max) continue;
         const uint32_t kfine = 1u << fb;
         p.local = true;
@@ -834,7 +837,7 @@ K1Params k1_params(const Weights& w, const Plan& p, uint64_t B, bool f32, const 
     kp.num_coarse = p.C;
     kp.num_tiles = p.T;
     kp.tile0 = 0;
-    kp.pad0 = 0;
+    kp.flags = p.ws_stage ? kK1StageKeys : 0u;
     kp.capc = p.capc;
     kp.n = p.n;
     return kp;
