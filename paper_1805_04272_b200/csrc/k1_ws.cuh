@@ -28,9 +28,6 @@ namespace mlsort {
 #ifndef MLSORT_K1_PREDW
 #define MLSORT_K1_PREDW 24
 #endif
-#ifndef MLSORT_K1_SCAN2
-#define MLSORT_K1_SCAN2 1       // thread-contiguous reservation scan (0: warp-serial rows; A/B)
-#endif
 constexpr int kPartWarps = MLSORT_K1_PARTW;   // (macros: warp-split experiments)
 constexpr int kPartThreads = kPartWarps * 32;     // 256
 constexpr int kClasses = 64;
@@ -341,65 +338,6 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
         // rbase[c] (sampled sizes, K0, or exact ones: the retry after an overflow).  A piece that would overflow
         // its region is marked kOverflowBase and not stored; the call then retries with exact
         // regions from the final cursors.
-#if MLSORT_K1_SCAN2
-        // Each partition thread owns cpt consecutive buckets: a block scan (partition warps
-        // only) of the per-thread totals places them in the staged tile, then they are reserved
-        // 16 at a time with their atomics issued back to back (one round trip of latency per 16
-        // buckets instead of per 32-bucket row of a warp-serial scan).
-        {
-            const uint32_t C4 = k1ws_c2(C);                    // multiple of 4 (zeroed tail)
-            const uint32_t cpt = ((C4 + kPartThreads - 1) / kPartThreads + 3u) & ~3u;
-            const uint32_t c0 = min(C4, (uint32_t)pt * cpt), c1 = min(C4, c0 + cpt);
-            uint32_t tot = 0;
-            for (uint32_t c = c0; c < c1; c += 4) {
-                const uint4 q = *reinterpret_cast<const uint4*>(hist + c);
-                tot += q.x + q.y + q.z + q.w;
-            }
-            uint32_t x = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t yy = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += yy;
-            }
-            if (lane == 31) scratch[pw] = x;
-            nbar_sync(kPart, kPartThreads);
-            uint32_t run = x - tot;
-            for (int w = 0; w < pw; ++w) run += scratch[w];
-            constexpr uint32_t kB = 16;
-            for (uint32_t cb = c0; cb < c1; cb += kB) {
-                uint32_t v[kB], g[kB];
-#pragma unroll
-                for (uint32_t j = 0; j < kB; j += 4) {
-                    if (cb + j < c1) {
-                        const uint4 q = *reinterpret_cast<const uint4*>(hist + cb + j);
-                        v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
-                    } else {
-                        v[j] = v[j + 1] = v[j + 2] = v[j + 3] = 0u;
-                    }
-                }
-#pragma unroll
-                for (uint32_t j = 0; j < kB; ++j) g[j] = v[j] ? atomicAdd(&cursor[cb + j], v[j]) : 0u;
-#pragma unroll
-                for (uint32_t j = 0; j < kB; ++j) {
-                    const uint32_t c = cb + j;
-                    if (c < c1) {
-                        hist[c] = run;
-                        if (c < C) {
-                            // region capacity: capc (fixed layout) or rbase[c+1] - rbase[c]
-                            // (sampled / exact layouts, K0 / the retry)
-                            const unsigned long long rcap =
-                                rbase ? rbase[c + 1] - rbase[c] : (unsigned long long)p.capc;
-                            const bool fits = (unsigned long long)g[j] + v[j] <= rcap;
-                            over |= !fits;
-                            const long long rb = rbase ? (long long)rbase[c] : (long long)c * p.capc;
-                            gbase[c] = fits ? rb + (long long)g[j] - (long long)run : kOverflowBase;
-                        }
-                        run += v[j];
-                    }
-                }
-            }
-        }
-#else
         {
             const uint32_t chunk = (C + kPartWarps - 1) / kPartWarps;
             const uint32_t b0 = min(C, (uint32_t)pw * chunk), b1 = min(C, b0 + chunk);
@@ -438,7 +376,6 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
                     if (gbase[c] != kOverflowBase) gbase[c] -= (long long)add;
                 }
         }
-#endif
         nbar_sync(kPart, kPartThreads);
         // ---- stage the tile partitioned by coarse id (position -> original offset e, key)
 #pragma unroll 4
