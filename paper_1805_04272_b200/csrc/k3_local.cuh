@@ -63,6 +63,7 @@ struct K3LParams {
     uint32_t to_mid;        // too-large buckets go to mid_list (1, primary of two passes) or to
                             // K4's big_list (0)
     uint32_t item_cap;      // ITEMS pass: capacity of the item list (k3_big.cuh)
+    uint32_t fshift;        // coarse-bucket passes: rank bucket = fine id >> fshift (experiments)
 };
 
 // The rank-bucket histogram holds two u16 counters per 32-bit word (a coarse bucket never
@@ -383,7 +384,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         K3L_T(0);
         const uint32_t t = ctrl[1];
         if (t >= items) break;
-        uint32_t c, n, nreg, f_lo = 0u, kf = p.kfine;
+        uint32_t c, n, nreg, f_lo = 0u, kf = ITEMS ? p.kfine : (p.kfine >> p.fshift);
         unsigned long long S0;
         if (ITEMS) {
             const K3Item it = item_list[t];
@@ -461,9 +462,9 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         const uint4* g8 = reinterpret_cast<const uint4*>(gf);
         // rank bucket of a region element inside this work item (ITEMS: f - f_lo, else f);
         // >= kf means "not in this item" (unsigned compare)
-        auto rel = [&](uint32_t f) { return ITEMS ? f - f_lo : f; };
+        auto rel = [&](uint32_t f) { return ITEMS ? f - f_lo : (f >> p.fshift); };
         auto hinc8 = [&](const uint4 v) {
-            if (!ITEMS) {
+            if (!ITEMS && p.fshift == 0) {
                 hist_add8(h2, v);
             } else {
                 const uint32_t w4[4] = {v.x, v.y, v.z, v.w};

@@ -638,6 +638,10 @@ cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_k
     kp.secondary = secondary ? 1u : 0u;
     kp.to_mid = to_mid ? 1u : 0u;
     kp.item_cap = p.item_cap;
+    {   // MLSORT_K3_FSHIFT=k: coarser rank buckets in the coarse-bucket passes (experiments)
+        const char* e = std::getenv("MLSORT_K3_FSHIFT");
+        kp.fshift = e ? (uint32_t)std::atoi(e) : 0u;
+    }
     DevStatus* st = at<DevStatus>(ws, L.status);
     unsigned long long* ticket = ITEMS ? &st->ticket3d : (secondary ? &st->ticket3b : &st->ticket3);
     kern<<<grid, NT, smem, s>>>(kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
