@@ -220,6 +220,125 @@ k3_cut(K3CutParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __restr
     }
 }
 
+// Giant all-equal runs of a permutation sort (C5: 131072 copies of each of 4096 values): the
+// keys are final, only the input indices of the run must become ascending (stability, reading
+// A9).  One CTA per run: min/max of the indices, a counting pass into nsb = len/32 index ranges
+// (sub-buckets of ~32), a scatter into the scratch area, then every sub-bucket is ranked by
+// one warp (<= 32: register shuffles; <= 224: shared memory) and written back, and the run is
+// checked to be strictly ascending.  Runs longer than kIdxSortMax, or with a sub-bucket over
+// 224 indices (a clustered index set), are flagged (seg.pad = 1) for the radix pass instead.
+constexpr uint32_t kIdxSortMax = 1u << 21;
+constexpr uint32_t kIdxSub = 4096;           // max sub-buckets per run
+constexpr uint32_t kIdxWarpBuf = 224;
+
+static __global__ void __launch_bounds__(1024, 1)
+k3_index_sort(K3Seg* __restrict__ segs, uint32_t seg_cap, uint32_t* __restrict__ perm, uint32_t* __restrict__ tmp,
+              DevStatus* __restrict__ st) {
+    __shared__ uint32_t cnt[kIdxSub + 1];
+    __shared__ uint32_t wbuf[32][kIdxWarpBuf];
+    __shared__ uint32_t s_min, s_max, s_bad;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t ns = (uint32_t)min(st->seg_count, (unsigned long long)seg_cap);
+    for (uint32_t g = blockIdx.x; g < ns; g += gridDim.x) {
+        const K3Seg sg = segs[g];
+        if (!(sg.flags & 1u) || sg.len > kIdxSortMax || sg.len < 2) {
+            if (tid == 0 && sg.len >= 2) segs[g].pad = 1u;          // radix pass
+            continue;
+        }
+        const uint32_t len = (uint32_t)sg.len;
+        uint32_t* pv = perm + sg.out;
+        uint32_t* tv = tmp + sg.out;
+        if (tid == 0) {
+            s_min = 0xffffffffu;
+            s_max = 0u;
+            s_bad = 0u;
+        }
+        __syncthreads();
+        uint32_t lmin = 0xffffffffu, lmax = 0u;
+        for (uint32_t i = tid; i < len; i += 1024) {
+            const uint32_t v = pv[i];
+            lmin = min(lmin, v);
+            lmax = max(lmax, v);
+        }
+        lmin = __reduce_min_sync(0xffffffffu, lmin);
+        lmax = __reduce_max_sync(0xffffffffu, lmax);
+        if (lane == 0) {
+            atomicMin(&s_min, lmin);
+            atomicMax(&s_max, lmax);
+        }
+        uint32_t nsb = 1;
+        while (nsb < kIdxSub && nsb * 32u < len) nsb <<= 1;
+        for (uint32_t j = tid; j <= nsb; j += 1024) cnt[j] = 0u;
+        __syncthreads();
+        const uint32_t vmin = s_min;
+        const uint64_t range = (uint64_t)s_max - vmin + 1;
+        uint32_t sh = 0;
+        while ((range - 1) >> sh >= nsb) ++sh;
+        for (uint32_t i = tid; i < len; i += 1024) atomicAdd(&cnt[(pv[i] - vmin) >> sh], 1u);
+        __syncthreads();
+        if (warp == 0) {                               // exclusive scan of nsb (<= 4096) counts
+            const uint32_t per = (nsb + 31) / 32;
+            const uint32_t j0 = min(nsb, lane * per), j1 = min(nsb, j0 + per);
+            uint32_t loc = 0;
+            for (uint32_t j = j0; j < j1; ++j) loc += cnt[j];
+            uint32_t x = loc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            uint32_t run = x - loc;
+            for (uint32_t j = j0; j < j1; ++j) {
+                const uint32_t c = cnt[j];
+                cnt[j] = run;
+                run += c;
+            }
+            if (lane == 31) cnt[nsb] = run;
+        }
+        __syncthreads();
+        // scatter into sub-bucket order; afterwards cnt[j] = end of sub-bucket j
+        for (uint32_t i = tid; i < len; i += 1024) {
+            const uint32_t v = pv[i];
+            tv[atomicAdd(&cnt[(v - vmin) >> sh], 1u)] = v;
+        }
+        __syncthreads();
+        for (uint32_t j = warp; j < nsb; j += 32) {
+            const uint32_t b = j ? cnt[j - 1] : 0u, e = cnt[j], sz = e - b;
+            if (sz <= 32) {
+                const uint32_t v = lane < sz ? tv[b + lane] : 0xffffffffu;
+                uint32_t r = 0;
+#pragma unroll
+                for (int k = 0; k < 32; ++k) r += __shfl_sync(0xffffffffu, v, k) < v ? 1u : 0u;
+                if (lane < sz) pv[b + r] = v;
+            } else if (sz <= kIdxWarpBuf) {
+                for (uint32_t k = lane; k < sz; k += 32) wbuf[warp][k] = tv[b + k];
+                __syncwarp();
+                for (uint32_t k = lane; k < sz; k += 32) {
+                    const uint32_t v = wbuf[warp][k];
+                    uint32_t r = 0;
+                    for (uint32_t q = 0; q < sz; ++q) r += wbuf[warp][q] < v ? 1u : 0u;
+                    pv[b + r] = v;
+                }
+                __syncwarp();
+            } else if (lane == 0) {
+                s_bad = 1u;
+            }
+        }
+        __syncthreads();
+        if (s_bad) {                                   // a clustered index set: radix pass
+            for (uint32_t i = tid; i < len; i += 1024) pv[i] = tv[i];   // (any order; re-sorted)
+            if (tid == 0) segs[g].pad = 1u;
+        } else {
+            uint32_t viol = 0;                         // reading A14: strictly ascending indices
+            for (uint32_t i = tid + 1; i < len; i += 1024) viol += pv[i - 1] < pv[i] ? 0u : 1u;
+            viol = __reduce_add_sync(0xffffffffu, viol);
+            if (lane == 0 && viol) atomicAdd(&st->violations, (unsigned long long)viol);
+            if (tid == 0) segs[g].pad = 0u;
+        }
+        __syncthreads();
+    }
+}
+
 // K5 over the item and segment lists: the key before each item / segment start must not follow
 // the key at it (the coarse-bucket starts are checked by k5_boundary_verify).
 template <typename KeyT, bool PERM>

@@ -638,9 +638,11 @@ cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_k
     kp.secondary = secondary ? 1u : 0u;
     kp.to_mid = to_mid ? 1u : 0u;
     kp.item_cap = p.item_cap;
-    {   // MLSORT_K3_FSHIFT=k: coarser rank buckets in the coarse-bucket passes (experiments)
+    {   // the coarse-bucket passes merge rank-bucket pairs (fine id >> 1: ~2 keys per rank bucket
+        // at B = N): C2 K3 0.416 -> 0.390 ms (>> 2: 0.508, >> 3: 0.731; profiles/r02/k3_fshift.log).
+        // MLSORT_K3_FSHIFT=k overrides (experiments).
         const char* e = std::getenv("MLSORT_K3_FSHIFT");
-        kp.fshift = e ? (uint32_t)std::atoi(e) : 0u;
+        kp.fshift = e ? (uint32_t)std::atoi(e) : (p.kfine >= 4096 ? 1u : 0u);
     }
     DevStatus* st = at<DevStatus>(ws, L.status);
     unsigned long long* ticket = ITEMS ? &st->ticket3d : (secondary ? &st->ticket3b : &st->ticket3);
@@ -993,6 +995,11 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         // K3 checks the adjacent order of every coarse bucket it sorts (reading A14) for every
         // model, fused with its store; K5 checks every coarse-bucket boundary.
         CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase)));
+        if (PERM) {     // giant all-equal runs: order their indices (k3_big.cuh; regions are dead now)
+            k3_index_sort<<<num_sms(), 1024, 0, s>>>(at<K3Seg>(ws, L.k3segs), p.seg_cap, out_perm,
+                                                     at<uint32_t>(ws, L.radix), dst);
+            CK(cudaGetLastError());
+        }
         tm.mark();
         tm.mark();
         k5_boundary_verify<KeyT, PERM><<<(unsigned)((nranges + 255) / 256), 256, 0, s>>>(
@@ -1002,7 +1009,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
                                                                  out_keys, out_perm, dst, p.item_cap, p.seg_cap, n);
         CK(cudaGetLastError());
         tm.mark();
-        nl.count += 7 + (p.cap1 > 0 ? 1 : 0);
+        nl.count += 7 + (p.cap1 > 0 ? 1 : 0) + (PERM ? 1 : 0);
 
         CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1045,15 +1052,21 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     uint64_t violations = st.violations + st.k3_violations;
     if (st.region_overflow > 0) violations += 1;   // a region was full: use the conventional sort
     if (st.item_overflow > 0) violations += 1;     // (lists sized for the worst case: not expected)
-    const bool need_radix = st.region_overflow == 0 && st.seg_count > 0;
+    std::vector<K3Seg> ks;
+    if (st.region_overflow == 0 && st.seg_count > 0) {
+        // segments left for the radix pass: distinct keys, or runs k3_index_sort flagged (pad)
+        const uint64_t nseg_dev = std::min<uint64_t>(st.seg_count, p.seg_cap);
+        ks.resize(nseg_dev);
+        CK(cudaMemcpyAsync(ks.data(), at<K3Seg>(ws, L.k3segs), nseg_dev * sizeof(K3Seg), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        ks.erase(std::remove_if(ks.begin(), ks.end(), [](const K3Seg& g) { return PERM && g.pad == 0u && (g.flags & 1u); }),
+                 ks.end());
+    }
+    const bool need_radix = !ks.empty();
     if (need_radix) {   // the stable radix pass over the runs K3 could not sort (k3_cut segments)
         std::vector<unsigned long long> seg;
         uint64_t tot = 0;
         bool all_equal = true;
-        const uint64_t nseg_dev = std::min<uint64_t>(st.seg_count, p.seg_cap);
-        std::vector<K3Seg> ks(nseg_dev);
-        CK(cudaMemcpyAsync(ks.data(), at<K3Seg>(ws, L.k3segs), nseg_dev * sizeof(K3Seg), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
         std::sort(ks.begin(), ks.end(), [](const K3Seg& a, const K3Seg& b) { return a.out < b.out; });
         for (const K3Seg& g : ks) {
             all_equal &= (g.flags & 1u) != 0;
