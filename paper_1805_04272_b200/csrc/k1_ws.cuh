@@ -40,7 +40,10 @@ struct WsCfg {
     static constexpr int kPredWarps = GROUP ? 16 : MLSORT_K1_PREDW;
     static constexpr int kThreads = (kPredWarps + kPartWarps) * 32;
     static constexpr int kPredThreads = kPredWarps * 32;
-    static constexpr int kKPT = sizeof(KeyT) == 4 ? 16 : 8;   // keys per predictor thread per tile
+    // keys per predictor thread per tile (f64 too: the per-tile partition work -- zeroing and
+    // scanning C counters, one reservation atomic per non-empty coarse bucket -- is amortised
+    // over more keys; f64 plans then run without key staging)
+    static constexpr int kKPT = 16;
     static constexpr int kT = kPredThreads * kKPT;
 };
 
@@ -50,18 +53,21 @@ __host__ __device__ constexpr int ws_tile(bool group = false) {
 }
 inline int ws_threads(bool group) { return group ? WsCfg<float, true>::kThreads : WsCfg<float, false>::kThreads; }
 
-// smem: sb[2][T] u32 | stage_key[T] KeyT (staged plans) | hist[C'] u32 | gbase[C'] i64 | stage_e[T] u16 |
+// smem: sb[2][T] u32 | stage_key[T] KeyT (staged plans) | hist[C'] u32 | gbase[C'] u32 | stage_e[T] u16 |
 //       (GROUP: cls_u[T] f32 | cls_e[T] u16 | chist[64] | ccur[64] | lut[2048] u8) | scratch
 // (C' = C rounded up to a multiple of 4 so every array stays 16-B aligned).  Without key staging
 // (K1Params::flags bit0 clear: plans whose C does not leave room for it) the piece stores
 // re-read each key from the tile in global memory (L2-resident) instead of shared memory.
 __host__ __device__ inline uint32_t k1ws_c2(uint32_t num_coarse) { return (num_coarse + 3u) & ~3u; }
 inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse, bool group = false, bool stage = true) {
-    return (size_t)tile * 8 + (stage ? (size_t)tile * ks : 0) + (size_t)k1ws_c2(num_coarse) * 12 + (size_t)tile * 2 +
+    return (size_t)tile * 8 + (stage ? (size_t)tile * ks : 0) + (size_t)k1ws_c2(num_coarse) * 8 + (size_t)tile * 2 +
            (group ? (size_t)tile * 6 + kClasses * 8 + 2048 : 0) + 256;
 }
 constexpr uint32_t kK1StageKeys = 1u;      // K1Params::flags
-constexpr long long kOverflowBase = LLONG_MIN;   // gbase marker of a piece that overflowed its region
+// gbase[c] holds (region slot of the tile's staged position 0) + T, so it is never negative and a
+// staged element at position pos goes to gbase[c] + pos - T; region slots + T stay below 2^32 - 1
+// (checked by the plan), which leaves 0xFFFFFFFF free as the marker of an overflowed piece.
+constexpr uint32_t kOverflowBase = 0xFFFFFFFFu;
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -92,7 +98,7 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
     KeyT* stage_key = reinterpret_cast<KeyT*>(smem + (size_t)T * 8);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (size_t)T * 8 + (staged ? (size_t)T * sizeof(KeyT) : 0));
     const uint32_t C = p.num_coarse;
-    long long* gbase = reinterpret_cast<long long*>(hist + k1ws_c2(C));   // region slot of staged position 0
+    uint32_t* gbase = hist + k1ws_c2(C);                   // region slot of staged position 0, + T
     uint16_t* stage_e = reinterpret_cast<uint16_t*>(gbase + k1ws_c2(C));
     float* cls_u = reinterpret_cast<float*>(stage_e + T);                   // GROUP: u in class order
     uint16_t* cls_e = reinterpret_cast<uint16_t*>(cls_u + (GROUP ? T : 0));  // GROUP: tile offsets
@@ -362,7 +368,7 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
                     const bool fits = (unsigned long long)g + v <= rcap;
                     over |= !fits;
                     const long long rb = rbase ? (long long)rbase[c] : (long long)c * p.capc;
-                    gbase[c] = fits ? rb + (long long)g - (long long)ex : kOverflowBase;
+                    gbase[c] = fits ? (uint32_t)(rb + (long long)g + (long long)T - (long long)ex) : kOverflowBase;
                 }
                 carry += __shfl_sync(0xffffffffu, x, 31);
             }
@@ -373,7 +379,7 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
             if (add)
                 for (uint32_t c = b0 + lane; c < b1; c += 32) {
                     hist[c] += add;
-                    if (gbase[c] != kOverflowBase) gbase[c] -= (long long)add;
+                    if (gbase[c] != kOverflowBase) gbase[c] -= add;
                 }
         }
         nbar_sync(kPart, kPartThreads);
@@ -390,9 +396,9 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
         for (uint32_t pos = pt; pos < cnt; pos += kPartThreads) {
             const uint32_t e = stage_e[pos];
             const uint32_t b = sbb[e];
-            const long long gb = gbase[b >> fbits];
+            const uint32_t gb = gbase[b >> fbits];
             if (gb != kOverflowBase) {
-                const size_t dst = (size_t)(gb + (long long)pos);
+                const size_t dst = (size_t)gb + pos - T;
                 reg_keys[dst] = staged ? stage_key[pos] : keys[base + e];
                 reg_fine[dst] = (uint16_t)(b & fmask);
                 if (PERM) reg_idx[dst] = (uint32_t)(base + e);

@@ -374,7 +374,9 @@ Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws = tru
         size_t sm = k1ws_smem_bytes(ks, wt, p.C, group, true);
         p.ws_stage = sm <= kK1WsSmemMax && !std::getenv("MLSORT_NO_STAGE");
         if (!p.ws_stage) sm = k1ws_smem_bytes(ks, wt, p.C, group, false);
-        if (sm <= kK1WsSmemMax) {
+        // k1_ws keeps 32-bit region slots (+ tile) with 0xFFFFFFFF reserved
+        const bool slots32 = p.area + p.tile + (uint64_t)wt + 8 < 0xFFFFFFFFull;
+        if (sm <= kK1WsSmemMax && slots32) {
             p.ws = true;
             p.ws_group = group;
             p.tile = wt;
