@@ -45,6 +45,38 @@ using namespace mlsort;
 namespace MLSORT_LOCAL {}
 using namespace MLSORT_LOCAL;
 
+// NVTX phase ranges (nvtx3 is header-only: no cost unless a profiler injects itself)
+#include <nvtx3/nvToolsExt.h>
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, size): a driver call per
+// launch would add host time in front of every sort
+template <typename F>
+cudaError_t set_smem(F* kern, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, size_t>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(kern) ^ ((uintptr_t)dev << 56));
+    for (auto& d : done)
+        if (d.first == key && d.second >= bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) {
+        bool found = false;
+        for (auto& d : done)
+            if (d.first == key) {
+                d.second = bytes;
+                found = true;
+            }
+        if (!found) done.emplace_back(key, bytes);
+    }
+    return e;
+}
+
 #define CK(x)                                                                                   \
     do {                                                                                        \
         cudaError_t e_ = (x);                                                                   \
@@ -565,7 +597,7 @@ cudaError_t launch_k1_t(const Plan& p, const KeyT* keys, const FoldedWeights& fw
                         void* ws, const Layout& L, cudaStream_t s, const uint32_t* bucket_in,
                         const uint32_t* idx_in, uint32_t b_lo, const unsigned long long* rbase) {
     auto kern = k1_predict_partition<KeyT, MPAD, PRED, PERM, GIVEN, kTileSmall>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k1_smem);
+    cudaError_t e = set_smem(kern, p.k1_smem);
     if (e != cudaSuccess) return e;
     kern<<<kp.num_tiles, kThreads, p.k1_smem, s>>>(keys, fw, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
                                           PERM ? at<uint32_t>(ws, L.reg_idx) : nullptr,
@@ -585,7 +617,7 @@ cudaError_t launch_k1_ws_t(const Plan& p, const KeyT* keys, const FoldedWeights&
     const bool group = PRED == kPredPacked && p.ws_group;
     auto kern = group ? k1_ws<KeyT, MPAD, PRED, PERM, 8, true, PRED == kPredPacked>
                       : k1_ws<KeyT, MPAD, PRED, PERM, kK1Kg, true, false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k1_smem);
+    cudaError_t e = set_smem(kern, p.k1_smem);
     if (e != cudaSuccess) return e;
     const int grid = std::min<int>(num_sms(), (int)kp.num_tiles);
     kern<<<grid, ws_threads(group), p.k1_smem, s>>>(keys, kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
@@ -630,7 +662,7 @@ cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_k
                            bool secondary, bool to_mid, uint32_t cap, size_t smem, int grid,
                            const unsigned long long* rbase) {
     auto kern = k3_local_sort<KeyT, PERM, NT, ITEMS>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     K3LParams kp;
     kp.capc = p.capc;
@@ -665,7 +697,7 @@ cudaError_t launch_k3_big(const Plan& p, void* ws, const Layout& L, KeyT* out_ke
     uint32_t gshift = 0;
     while ((p.kfine >> gshift) > kCutGroups) ++gshift;
     const size_t smem = (size_t)(2 * (p.kfine >> gshift) + 2) * 4;
-    cudaError_t e = cudaFuncSetAttribute(cut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_smem(cut, smem);
     if (e != cudaSuccess) return e;
     K3CutParams cp;
     cp.capc = p.capc;
@@ -734,8 +766,7 @@ int radix_sort_pairs(Bits* k0, uint32_t* v0, Bits* k1, uint32_t* v1, uint32_t* g
                      int key_bits = (int)(sizeof(Bits) * 8)) {
     const uint32_t nchunks = (uint32_t)((n + kRadixChunk - 1) / kRadixChunk);
     int cur = 0;
-    err = cudaFuncSetAttribute(k_radix_scatter<Bits>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)radix_scatter_smem<Bits>());
+    err = set_smem(k_radix_scatter<Bits>, radix_scatter_smem<Bits>());
     if (err != cudaSuccess) return 0;
     auto pass = [&](int field, int shift) {
         Bits* ki = cur ? k1 : k0;
@@ -914,7 +945,7 @@ cudaError_t launch_k0(const Plan& p, const KeyT* keys, uint32_t mpad, const Fold
     cudaError_t e = cudaSuccess;
 #define K0CASE(M)                                                                                          \
     if (mpad == M) {                                                                                       \
-        e = cudaFuncSetAttribute(k0_sample<KeyT, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        e = set_smem(k0_sample<KeyT, M>, smem);                                                            \
         if (e != cudaSuccess) return e;                                                                    \
         k0_sample<KeyT, M><<<grid, 256, smem, s>>>(keys, p.n, p.stride, fw, kp, at<uint32_t>(ws, L.est));  \
     }
@@ -932,6 +963,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
                  uint32_t* out_perm, void* ws, uint64_t ws_bytes, cudaStream_t s, mlsort_info* info,
                  const uint32_t* bucket_in, const uint32_t* idx_in, uint32_t b_lo, bool timing = false,
                  bool verify_all = false, const ChunkPlan* chunks = nullptr) {
+    NvtxRange nvtx_call("mlsort_sort");
     Launches nl;
     PhaseTimer tm;
     const bool group = !GIVEN && pred == kPredSkip;
@@ -987,6 +1019,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
             }
             nl.count -= 1;   // counted once below
         } else {
+            NvtxRange r("mlsort K1 predict + partition");
             CK((launch_k1<KeyT, PERM, GIVEN>(p, keys, mpad, pred, fw, kp, ws, L, s, bucket_in, idx_in, b_lo, rbase)));
         }
         tm.mark();
@@ -996,7 +1029,10 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         tm.mark();
         // K3 checks the adjacent order of every coarse bucket it sorts (reading A14) for every
         // model, fused with its store; K5 checks every coarse-bucket boundary.
-        CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase)));
+        {
+            NvtxRange r("mlsort K3 (passes, cut, rounds)");
+            CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase)));
+        }
         if (PERM) {     // giant all-equal runs: order their indices (k3_big.cuh; regions are dead now)
             k3_index_sort<<<num_sms(), 1024, 0, s>>>(at<K3Seg>(ws, L.k3segs), p.seg_cap, out_perm,
                                                      at<uint32_t>(ws, L.radix), dst);
@@ -1066,6 +1102,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     }
     const bool need_radix = !ks.empty();
     if (need_radix) {   // the stable radix pass over the runs K3 could not sort (k3_cut segments)
+        NvtxRange r("mlsort radix segments");
         std::vector<unsigned long long> seg;
         uint64_t tot = 0;
         bool all_equal = true;
