@@ -28,6 +28,9 @@ namespace mlsort {
 #ifndef MLSORT_K1_PREDW
 #define MLSORT_K1_PREDW 24
 #endif
+#ifndef MLSORT_K1_PHIST
+#define MLSORT_K1_PHIST 1      // predictor warps build the coarse histogram (0: partition warps; A/B)
+#endif
 constexpr int kPartWarps = MLSORT_K1_PARTW;   // (macros: warp-split experiments)
 constexpr int kPartThreads = kPartWarps * 32;     // 256
 constexpr int kClasses = 64;
@@ -54,14 +57,16 @@ __host__ __device__ constexpr int ws_tile(bool group = false) {
 inline int ws_threads(bool group) { return group ? WsCfg<float, true>::kThreads : WsCfg<float, false>::kThreads; }
 
 // smem: sb[2][T] u32 | stage_key[T] KeyT (staged plans) | hist[C'] u32 | gbase[C'] u32 | stage_e[T] u16 |
-//       (GROUP: cls_u[T] f32 | cls_e[T] u16 | chist[64] | ccur[64] | lut[2048] u8) | scratch
+//       (GROUP: cls_u[T] f32 | cls_e[T] u16 | chist[64] | ccur[64] | lut[2048] u8) |
+//       (plain, MLSORT_K1_PHIST: hp[2][C'/2] u32 = u16 counter pairs per buffer) | scratch
 // (C' = C rounded up to a multiple of 4 so every array stays 16-B aligned).  Without key staging
 // (K1Params::flags bit0 clear: plans whose C does not leave room for it) the piece stores
 // re-read each key from the tile in global memory (L2-resident) instead of shared memory.
 __host__ __device__ inline uint32_t k1ws_c2(uint32_t num_coarse) { return (num_coarse + 3u) & ~3u; }
 inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse, bool group = false, bool stage = true) {
     return (size_t)tile * 8 + (stage ? (size_t)tile * ks : 0) + (size_t)k1ws_c2(num_coarse) * 8 + (size_t)tile * 2 +
-           (group ? (size_t)tile * 6 + kClasses * 8 + 2048 : 0) + 256;
+           (group ? (size_t)tile * 6 + kClasses * 8 + 2048 : (MLSORT_K1_PHIST ? (size_t)k1ws_c2(num_coarse) * 4 : 0)) +
+           256;
 }
 constexpr uint32_t kK1StageKeys = 1u;      // K1Params::flags
 // gbase[c] holds (region slot of the tile's staged position 0) + T, so it is never negative and a
@@ -105,7 +110,12 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
     uint32_t* chist = reinterpret_cast<uint32_t*>(cls_e + (GROUP ? T : 0));
     uint32_t* ccur = chist + (GROUP ? kClasses : 0);
     unsigned char* lut = reinterpret_cast<unsigned char*>(ccur + (GROUP ? kClasses : 0));
-    uint32_t* scratch = reinterpret_cast<uint32_t*>(lut + (GROUP ? 2048 : 0));
+    // plain path: the predictor warps count each tile's coarse buckets into hp[buf] (two u16
+    // counters per word); the partition warps read and clear them in their scan
+    constexpr bool kPH = !GROUP && MLSORT_K1_PHIST;
+    uint32_t* hp = reinterpret_cast<uint32_t*>(lut + (GROUP ? 2048 : 0));
+    const uint32_t hpw = k1ws_c2(p.num_coarse) / 2;           // words per buffer
+    uint32_t* scratch = hp + (kPH ? 2 * hpw : 0);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -115,6 +125,10 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
         for (int i = tid; i < 2048 / 4; i += kWsThreads)
             reinterpret_cast<uint32_t*>(lut)[i] = reinterpret_cast<const uint32_t*>(fw.lut)[i];
         if (tid < kClasses) chist[tid] = 0u;
+        __syncthreads();
+    }
+    if (kPH) {
+        for (uint32_t i = tid; i < 2 * hpw; i += kWsThreads) hp[i] = 0u;
         __syncthreads();
     }
 
@@ -303,8 +317,15 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
                 gvm_forward_fxp<MPAD, PRED, kGroupWs, true>(fw, u, ul, y);
             uint32_t* sbb = sb + buf * T;
 #pragma unroll
-            for (int q = 0; q < kGroupWs; ++q)
-                sbb[tid + kPredThreads * (g * kGroupWs + q)] = bucket_of_fxp(y[q], p.bm);
+            for (int q = 0; q < kGroupWs; ++q) {
+                const uint32_t e = tid + kPredThreads * (g * kGroupWs + q);
+                const uint32_t b = bucket_of_fxp(y[q], p.bm);
+                sbb[e] = b;
+                if (kPH && e < cnt) {
+                    const uint32_t c = b >> p.fine_bits;
+                    atomicAdd(&hp[buf * hpw + (c >> 1)], 1u << ((c & 1u) << 4));
+                }
+            }
             if (g == G - 1) nbar_arrive(kFull0 + buf, kWsThreads);        // sb[buf] is ready
         }
         tail_lo = __reduce_add_sync(0xffffffffu, tail_lo);
@@ -328,16 +349,19 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
         const uint32_t cnt = (uint32_t)min((uint64_t)T, p.n - base);
         const int buf = k & 1;
         const uint32_t* sbb = sb + buf * T;
-        for (uint32_t c = pt; c < k1ws_c2(C); c += kPartThreads) hist[c] = 0u;
+        if (!kPH)
+            for (uint32_t c = pt; c < k1ws_c2(C); c += kPartThreads) hist[c] = 0u;
         nbar_sync(kFull0 + buf, kWsThreads);           // predictors finished tile k (also orders the zeroing)
         if (!PARTITION) {
             if (k + 2 < my_tiles) nbar_arrive(kEmpty0 + buf, kWsThreads);
             continue;
         }
-        // ---- coarse histogram
+        // ---- coarse histogram (plain path: already built by the predictor warps in hp[buf])
+        if (!kPH) {
 #pragma unroll 4
-        for (uint32_t e = pt; e < cnt; e += kPartThreads) atomicAdd(&hist[sbb[e] >> fbits], 1u);
-        nbar_sync(kPart, kPartThreads);
+            for (uint32_t e = pt; e < cnt; e += kPartThreads) atomicAdd(&hist[sbb[e] >> fbits], 1u);
+            nbar_sync(kPart, kPartThreads);
+        }
         // ---- scan (warp rows, conflict-free) + reservation of this tile's piece in every region.
         // gbase[c] = region slot of the tile's staged position 0 for coarse bucket c, so a staged
         // element at position pos goes to gbase[c] + pos.  Regions start at c * capc, or at
@@ -345,13 +369,23 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
         // its region is marked kOverflowBase and not stored; the call then retries with exact
         // regions from the final cursors.
         {
-            const uint32_t chunk = (C + kPartWarps - 1) / kPartWarps;
+            // (even chunks: a u16 counter pair of hp never straddles two warps)
+            const uint32_t chunk = (((C + kPartWarps - 1) / kPartWarps) + 1u) & ~1u;
             const uint32_t b0 = min(C, (uint32_t)pw * chunk), b1 = min(C, b0 + chunk);
             uint32_t carry = 0;
 #pragma unroll 4
             for (uint32_t r = b0; r < b1; r += 32) {
                 const uint32_t c = r + lane;
-                const uint32_t v = c < b1 ? hist[c] : 0u;
+                uint32_t v;
+                if (kPH) {                                     // read and clear the predictor's counters
+                    uint32_t* hw = &hp[buf * hpw + (c >> 1)];
+                    const uint32_t wv = c < b1 ? *hw : 0u;
+                    v = (wv >> ((c & 1u) << 4)) & 0xffffu;
+                    __syncwarp();
+                    if (c < b1 && !(c & 1u)) *hw = 0u;
+                } else {
+                    v = c < b1 ? hist[c] : 0u;
+                }
                 const uint32_t g = v ? atomicAdd(&cursor[c], v) : 0u;
                 uint32_t x = v;
 #pragma unroll
