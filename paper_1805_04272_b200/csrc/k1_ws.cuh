@@ -29,7 +29,9 @@ namespace mlsort {
 #define MLSORT_K1_PREDW 24
 #endif
 #ifndef MLSORT_K1_PHIST
-#define MLSORT_K1_PHIST 1      // predictor warps build the coarse histogram (0: partition warps; A/B)
+#define MLSORT_K1_PHIST 0      // 1: predictor warps build the coarse histogram (measured slower:
+                               // C2 K1 1.011 -> 1.043 ms, profiles/r02/ab_k1_phist.log -- K1 is
+                               // bound by the predictor warps' issue, so work moved there costs)
 #endif
 constexpr int kPartWarps = MLSORT_K1_PARTW;   // (macros: warp-split experiments)
 constexpr int kPartThreads = kPartWarps * 32;     // 256

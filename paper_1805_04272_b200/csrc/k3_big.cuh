@@ -222,7 +222,7 @@ k3_cut(K3CutParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __restr
 
 // Giant all-equal runs of a permutation sort (C5: 131072 copies of each of 4096 values): the
 // keys are final, only the input indices of the run must become ascending (stability, reading
-// A9).  One CTA per run: min/max of the indices, a counting pass into nsb = len/32 index ranges
+// A9).  One CTA (512 threads, three per SM) per run: min/max of the indices, a counting pass into nsb = len/32 index ranges
 // (sub-buckets of ~32), a scatter into the scratch area, then every sub-bucket is ranked by
 // one warp (<= 32: register shuffles; <= 224: shared memory) and written back, and the run is
 // checked to be strictly ascending.  Runs longer than kIdxSortMax, or with a sub-bucket over
@@ -231,11 +231,12 @@ constexpr uint32_t kIdxSortMax = 1u << 21;
 constexpr uint32_t kIdxSub = 4096;           // max sub-buckets per run
 constexpr uint32_t kIdxWarpBuf = 224;
 
-static __global__ void __launch_bounds__(1024, 1)
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 512 ? 3 : 1)
 k3_index_sort(K3Seg* __restrict__ segs, uint32_t seg_cap, uint32_t* __restrict__ perm, uint32_t* __restrict__ tmp,
               DevStatus* __restrict__ st) {
     __shared__ uint32_t cnt[kIdxSub + 1];
-    __shared__ uint32_t wbuf[32][kIdxWarpBuf];
+    __shared__ uint32_t wbuf[NT / 32][kIdxWarpBuf];
     __shared__ uint32_t s_min, s_max, s_bad;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t ns = (uint32_t)min(st->seg_count, (unsigned long long)seg_cap);
@@ -255,7 +256,7 @@ k3_index_sort(K3Seg* __restrict__ segs, uint32_t seg_cap, uint32_t* __restrict__
         }
         __syncthreads();
         uint32_t lmin = 0xffffffffu, lmax = 0u;
-        for (uint32_t i = tid; i < len; i += 1024) {
+        for (uint32_t i = tid; i < len; i += NT) {
             const uint32_t v = pv[i];
             lmin = min(lmin, v);
             lmax = max(lmax, v);
@@ -268,13 +269,13 @@ k3_index_sort(K3Seg* __restrict__ segs, uint32_t seg_cap, uint32_t* __restrict__
         }
         uint32_t nsb = 1;
         while (nsb < kIdxSub && nsb * 32u < len) nsb <<= 1;
-        for (uint32_t j = tid; j <= nsb; j += 1024) cnt[j] = 0u;
+        for (uint32_t j = tid; j <= nsb; j += NT) cnt[j] = 0u;
         __syncthreads();
         const uint32_t vmin = s_min;
         const uint64_t range = (uint64_t)s_max - vmin + 1;
         uint32_t sh = 0;
         while ((range - 1) >> sh >= nsb) ++sh;
-        for (uint32_t i = tid; i < len; i += 1024) atomicAdd(&cnt[(pv[i] - vmin) >> sh], 1u);
+        for (uint32_t i = tid; i < len; i += NT) atomicAdd(&cnt[(pv[i] - vmin) >> sh], 1u);
         __syncthreads();
         if (warp == 0) {                               // exclusive scan of nsb (<= 4096) counts
             const uint32_t per = (nsb + 31) / 32;
@@ -297,12 +298,12 @@ k3_index_sort(K3Seg* __restrict__ segs, uint32_t seg_cap, uint32_t* __restrict__
         }
         __syncthreads();
         // scatter into sub-bucket order; afterwards cnt[j] = end of sub-bucket j
-        for (uint32_t i = tid; i < len; i += 1024) {
+        for (uint32_t i = tid; i < len; i += NT) {
             const uint32_t v = pv[i];
             tv[atomicAdd(&cnt[(v - vmin) >> sh], 1u)] = v;
         }
         __syncthreads();
-        for (uint32_t j = warp; j < nsb; j += 32) {
+        for (uint32_t j = warp; j < nsb; j += NT / 32) {
             const uint32_t b = j ? cnt[j - 1] : 0u, e = cnt[j], sz = e - b;
             if (sz <= 32) {
                 const uint32_t v = lane < sz ? tv[b + lane] : 0xffffffffu;
@@ -326,11 +327,11 @@ k3_index_sort(K3Seg* __restrict__ segs, uint32_t seg_cap, uint32_t* __restrict__
         }
         __syncthreads();
         if (s_bad) {                                   // a clustered index set: radix pass
-            for (uint32_t i = tid; i < len; i += 1024) pv[i] = tv[i];   // (any order; re-sorted)
+            for (uint32_t i = tid; i < len; i += NT) pv[i] = tv[i];   // (any order; re-sorted)
             if (tid == 0) segs[g].pad = 1u;
         } else {
             uint32_t viol = 0;                         // reading A14: strictly ascending indices
-            for (uint32_t i = tid + 1; i < len; i += 1024) viol += pv[i - 1] < pv[i] ? 0u : 1u;
+            for (uint32_t i = tid + 1; i < len; i += NT) viol += pv[i - 1] < pv[i] ? 0u : 1u;
             viol = __reduce_add_sync(0xffffffffu, viol);
             if (lane == 0 && viol) atomicAdd(&st->violations, (unsigned long long)viol);
             if (tid == 0) segs[g].pad = 0u;

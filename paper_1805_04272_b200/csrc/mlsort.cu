@@ -1034,7 +1034,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
             CK((launch_k3<KeyT, PERM>(p, ws, L, out_keys, out_perm, s, rbase)));
         }
         if (PERM) {     // giant all-equal runs: order their indices (k3_big.cuh; regions are dead now)
-            k3_index_sort<<<num_sms(), 1024, 0, s>>>(at<K3Seg>(ws, L.k3segs), p.seg_cap, out_perm,
+            k3_index_sort<512><<<num_sms() * 3, 512, 0, s>>>(at<K3Seg>(ws, L.k3segs), p.seg_cap, out_perm,
                                                      at<uint32_t>(ws, L.radix), dst);
             CK(cudaGetLastError());
         }
