@@ -33,16 +33,20 @@ namespace mlsort {
                                // C2 K1 1.011 -> 1.043 ms, profiles/r02/ab_k1_phist.log -- K1 is
                                // bound by the predictor warps' issue, so work moved there costs)
 #endif
+#ifndef MLSORT_K1_GROUP24
+#define MLSORT_K1_GROUP24 1    // grouped variant: 24 predictor warps, u re-read from the keys (0: 16 warps, u in smem)
+#endif
 constexpr int kPartWarps = MLSORT_K1_PARTW;   // (macros: warp-split experiments)
 constexpr int kPartThreads = kPartWarps * 32;     // 256
 constexpr int kClasses = 64;
 
 // Warp split and tile of one k1_ws variant.  Plain: 24 predictor warps (1024 threads, 64
-// registers).  GROUP: 16 predictor warps (768 threads, up to 85 registers) and a smaller tile,
-// which leaves room for the tile's u values in class order.
+// registers).  GROUP: 24 predictor warps too (MLSORT_K1_GROUP24): the class order keeps only
+// the tile offsets in shared memory and phase D re-reads each key from the tile in global
+// memory (L2-resident); 16 warps and u in shared memory otherwise.
 template <typename KeyT, bool GROUP>
 struct WsCfg {
-    static constexpr int kPredWarps = GROUP ? 16 : MLSORT_K1_PREDW;
+    static constexpr int kPredWarps = GROUP ? (MLSORT_K1_GROUP24 ? 24 : 16) : MLSORT_K1_PREDW;
     static constexpr int kThreads = (kPredWarps + kPartWarps) * 32;
     static constexpr int kPredThreads = kPredWarps * 32;
     // keys per predictor thread per tile (f64 too: the per-tile partition work -- zeroing and
@@ -67,7 +71,8 @@ inline int ws_threads(bool group) { return group ? WsCfg<float, true>::kThreads 
 __host__ __device__ inline uint32_t k1ws_c2(uint32_t num_coarse) { return (num_coarse + 3u) & ~3u; }
 inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse, bool group = false, bool stage = true) {
     return (size_t)tile * 8 + (stage ? (size_t)tile * ks : 0) + (size_t)k1ws_c2(num_coarse) * 8 + (size_t)tile * 2 +
-           (group ? (size_t)tile * 6 + kClasses * 8 + 2048 : (MLSORT_K1_PHIST ? (size_t)k1ws_c2(num_coarse) * 4 : 0)) +
+           (group ? (size_t)tile * (MLSORT_K1_GROUP24 ? 2 : 6) + kClasses * 8 + 2048
+                  : (MLSORT_K1_PHIST ? (size_t)k1ws_c2(num_coarse) * 4 : 0)) +
            256;
 }
 constexpr uint32_t kK1StageKeys = 1u;      // K1Params::flags
@@ -107,8 +112,9 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
     const uint32_t C = p.num_coarse;
     uint32_t* gbase = hist + k1ws_c2(C);                   // region slot of staged position 0, + T
     uint16_t* stage_e = reinterpret_cast<uint16_t*>(gbase + k1ws_c2(C));
-    float* cls_u = reinterpret_cast<float*>(stage_e + T);                   // GROUP: u in class order
-    uint16_t* cls_e = reinterpret_cast<uint16_t*>(cls_u + (GROUP ? T : 0));  // GROUP: tile offsets
+    constexpr bool kClsU = GROUP && !MLSORT_K1_GROUP24;
+    float* cls_u = reinterpret_cast<float*>(stage_e + T);                   // GROUP (16 warps): u in class order
+    uint16_t* cls_e = reinterpret_cast<uint16_t*>(cls_u + (kClsU ? T : 0));  // GROUP: tile offsets
     uint32_t* chist = reinterpret_cast<uint32_t*>(cls_e + (GROUP ? T : 0));
     uint32_t* ccur = chist + (GROUP ? kClasses : 0);
     unsigned char* lut = reinterpret_cast<unsigned char*>(ccur + (GROUP ? kClasses : 0));
@@ -204,7 +210,7 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
                 const uint32_t c = (cls4[i >> 2] >> ((i & 3) * 8)) & 0xffu;
                 if (c < kClasses) {
                     const uint32_t pos = atomicAdd(&ccur[c], 1u);
-                    cls_u[pos] = ua[i];
+                    if (kClsU) cls_u[pos] = ua[i];
                     cls_e[pos] = (uint16_t)(tid + kPredThreads * i);
                 }
             }
@@ -220,12 +226,30 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
                 int32_t y[kGroupWs];
                 float mn = INFINITY, mx = -INFINITY;
                 bool safe = true;
+                KeyT xg[kGroupWs];
+                if (!kClsU) {                                    // gather the group's keys (L2)
+#pragma unroll
+                    for (int q = 0; q < kGroupWs; ++q) {
+                        const uint32_t pos = (uint32_t)warp * (KPT * 32) + (g * kGroupWs + q) * 32 + lane;
+                        ec[q] = pos < cnt ? (uint32_t)cls_e[pos] : 0xffffffffu;
+                    }
+#pragma unroll
+                    for (int q = 0; q < kGroupWs; ++q) xg[q] = ec[q] != 0xffffffffu ? keys[base + ec[q]] : (KeyT)p.lo_d;
+                }
 #pragma unroll
                 for (int q = 0; q < kGroupWs; ++q) {
                     const uint32_t pos = (uint32_t)warp * (KPT * 32) + (g * kGroupWs + q) * 32 + lane;
                     const bool valid = pos < cnt;
-                    u[q] = valid ? cls_u[pos] : 0.0f;
-                    ec[q] = valid ? (uint32_t)cls_e[pos] : 0xffffffffu;
+                    if (kClsU) {
+                        u[q] = valid ? cls_u[pos] : 0.0f;
+                        ec[q] = valid ? (uint32_t)cls_e[pos] : 0xffffffffu;
+                    } else {                                     // the same u as phase A
+                        KeyT x = xg[q];
+                        if (!KeyTraits<KeyT>::finite(x)) x = (KeyT)p.lo_d;
+                        float ulo;
+                        key_to_u<KeyT>(x, p, u[q], ulo);
+                        if (!valid) u[q] = 0.0f;
+                    }
                     ul[q] = 0.0f;
                     if (valid) {
                         mn = fminf(mn, u[q]);
