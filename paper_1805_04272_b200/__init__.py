@@ -19,7 +19,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libmlsort.so")
+# MLSORT_LIB: load a prebuilt variant library instead (A/B experiments; never built here)
+_LIB_PATH = os.environ.get("MLSORT_LIB") or os.path.join(_HERE, "libmlsort.so")
 _lib = None
 
 F32, F64 = 0, 1
@@ -72,7 +73,7 @@ def lib():
     """Load libmlsort.so (build it in-tree first if it is missing or stale)."""
     global _lib
     if _lib is None:
-        if os.environ.get("MLSORT_NO_BUILD") != "1":
+        if os.environ.get("MLSORT_NO_BUILD") != "1" and not os.environ.get("MLSORT_LIB"):
             from . import build as _b
             if _b.needs_build():
                 _b.build()

@@ -9,7 +9,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-LIB = os.path.join(HERE, "libmlsort.so")
+# MLSORT_LIB_OUT: build a variant library elsewhere (A/B experiments; objects in their own dir)
+LIB = os.environ.get("MLSORT_LIB_OUT") or os.path.join(HERE, "libmlsort.so")
+OBJDIR = os.path.join(CSRC, "build" + ("_" + os.path.basename(LIB).replace(".so", "") if os.environ.get("MLSORT_LIB_OUT") else ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 # (source, object suffix, extra flags): mlsort.cu is compiled once per translation-unit slice
@@ -43,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     procs = []
     for src, suffix, extra in SOURCES:
-        obj = os.path.join(CSRC, "build", src + (("." + suffix) if suffix else "") + ".o")
+        obj = os.path.join(OBJDIR, src + (("." + suffix) if suffix else "") + ".o")
         os.makedirs(os.path.dirname(obj), exist_ok=True)
         if src.endswith(".cu"):
             cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,

@@ -70,7 +70,7 @@ k_dist_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Pa
             xs[q] = x;
             key_to_u<KeyT>(x, p, u[q], ul[q]);
         }
-        gvm_forward_fxp<MPAD, PRED, G8>(fw, u, ul, y);
+        gvm_forward_dense<MPAD, PRED, G8>(fw, u, ul, y);
 #pragma unroll
         for (int q = 0; q < G8; ++q) {
             const uint64_t e = base + tid + (uint64_t)kRadixThreads * (g * G8 + q);

@@ -37,7 +37,7 @@ k0_sample(const KeyT* __restrict__ keys, uint64_t n, uint64_t stride, FoldedWeig
             if (!KeyTraits<KeyT>::finite(x)) x = (KeyT)p.lo_d;
             key_to_u<KeyT>(x, p, u[q], ul[q]);
         }
-        gvm_forward_fxp<MPAD, kPredPacked, G>(fw, u, ul, y);
+        gvm_forward_dense<MPAD, kPredPacked, G>(fw, u, ul, y);
 #pragma unroll
         for (int q = 0; q < G; ++q)
             if (s0 + (uint64_t)q * step < ns) atomicAdd(&h[bucket_of_fxp(y[q], p.bm) >> p.fine_bits], 1u);

@@ -146,7 +146,7 @@ k1_predict_partition(const KeyT* __restrict__ keys, FoldedWeights fw, K1Params p
             }
             key_to_u<KeyT>(x, p, u[q], ul[q]);
         }
-        gvm_forward_fxp<MPAD, PRED, kGroup>(fw, u, ul, y);
+        gvm_forward_dense<MPAD, PRED, kGroup>(fw, u, ul, y);
 #pragma unroll
         for (int q = 0; q < kGroup; ++q) sb[tid + kThreads * (g * kGroup + q)] = bucket_of_fxp(y[q], p.bm);
     }

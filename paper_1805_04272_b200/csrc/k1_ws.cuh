@@ -15,6 +15,7 @@
 #pragma once
 
 #include <climits>
+#include <type_traits>
 
 #include "common.cuh"
 #include "predict.cuh"
@@ -27,11 +28,6 @@ namespace mlsort {
 #endif
 #ifndef MLSORT_K1_PREDW
 #define MLSORT_K1_PREDW 24
-#endif
-#ifndef MLSORT_K1_PHIST
-#define MLSORT_K1_PHIST 0      // 1: predictor warps build the coarse histogram (measured slower:
-                               // C2 K1 1.011 -> 1.043 ms, profiles/r02/ab_k1_phist.log -- K1 is
-                               // bound by the predictor warps' issue, so work moved there costs)
 #endif
 #ifndef MLSORT_K1_GROUP24
 #define MLSORT_K1_GROUP24 1    // grouped variant: 24 predictor warps, u re-read from the keys (0: 16 warps, u in smem)
@@ -63,16 +59,14 @@ __host__ __device__ constexpr int ws_tile(bool group = false) {
 inline int ws_threads(bool group) { return group ? WsCfg<float, true>::kThreads : WsCfg<float, false>::kThreads; }
 
 // smem: sb[2][T] u32 | stage_key[T] KeyT (staged plans) | hist[C'] u32 | gbase[C'] u32 | stage_e[T] u16 |
-//       (GROUP: cls_u[T] f32 | cls_e[T] u16 | chist[64] | ccur[64] | lut[2048] u8) |
-//       (plain, MLSORT_K1_PHIST: hp[2][C'/2] u32 = u16 counter pairs per buffer) | scratch
+//       (GROUP: cls_u[T] f32 | cls_e[T] u16 | chist[64] | ccur[64] | lut[2048] u8) | scratch
 // (C' = C rounded up to a multiple of 4 so every array stays 16-B aligned).  Without key staging
 // (K1Params::flags bit0 clear: plans whose C does not leave room for it) the piece stores
 // re-read each key from the tile in global memory (L2-resident) instead of shared memory.
 __host__ __device__ inline uint32_t k1ws_c2(uint32_t num_coarse) { return (num_coarse + 3u) & ~3u; }
 inline size_t k1ws_smem_bytes(size_t ks, uint32_t tile, uint32_t num_coarse, bool group = false, bool stage = true) {
     return (size_t)tile * 8 + (stage ? (size_t)tile * ks : 0) + (size_t)k1ws_c2(num_coarse) * 8 + (size_t)tile * 2 +
-           (group ? (size_t)tile * (MLSORT_K1_GROUP24 ? 2 : 6) + kClasses * 8 + 2048
-                  : (MLSORT_K1_PHIST ? (size_t)k1ws_c2(num_coarse) * 4 : 0)) +
+           (group ? (size_t)tile * (MLSORT_K1_GROUP24 ? 2 : 6) + kClasses * 8 + 2048 : 0) +
            256;
 }
 constexpr uint32_t kK1StageKeys = 1u;      // K1Params::flags
@@ -118,12 +112,7 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
     uint32_t* chist = reinterpret_cast<uint32_t*>(cls_e + (GROUP ? T : 0));
     uint32_t* ccur = chist + (GROUP ? kClasses : 0);
     unsigned char* lut = reinterpret_cast<unsigned char*>(ccur + (GROUP ? kClasses : 0));
-    // plain path: the predictor warps count each tile's coarse buckets into hp[buf] (two u16
-    // counters per word); the partition warps read and clear them in their scan
-    constexpr bool kPH = !GROUP && MLSORT_K1_PHIST;
-    uint32_t* hp = reinterpret_cast<uint32_t*>(lut + (GROUP ? 2048 : 0));
-    const uint32_t hpw = k1ws_c2(p.num_coarse) / 2;           // words per buffer
-    uint32_t* scratch = hp + (kPH ? 2 * hpw : 0);
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(lut + (GROUP ? 2048 : 0));
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -133,10 +122,6 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
         for (int i = tid; i < 2048 / 4; i += kWsThreads)
             reinterpret_cast<uint32_t*>(lut)[i] = reinterpret_cast<const uint32_t*>(fw.lut)[i];
         if (tid < kClasses) chist[tid] = 0u;
-        __syncthreads();
-    }
-    if (kPH) {
-        for (uint32_t i = tid; i < 2 * hpw; i += kWsThreads) hp[i] = 0u;
         __syncthreads();
     }
 
@@ -286,6 +271,8 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
         // The (tile, group) sequence is flattened so the keys of the next group -- possibly
         // the first group of the next tile -- are loaded while the current group is evaluated.
         constexpr int G = KPT / kGroupWs;                  // groups per tile
+        // (128-bit key loads / bucket stores here need quad-aligned registers and made this
+        // 64-register kernel spill: scalar, coalesced across the warp)
         uint32_t tail_lo = 0, tail_hi = 0;
         const uint32_t nsteps = my_tiles * G;
         KeyT xn[kGroupWs];
@@ -311,47 +298,58 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
 #pragma unroll
             for (int q = 0; q < kGroupWs; ++q) xc[q] = xn[q];
             if (step + 1 < nsteps) load_group(step + 1);
+            // validation (A0) and tail counts: a warp whose keys are all inside [input_lo,
+            // input_hi] (finite, no tail; padding keys are input_lo) skips both
+            bool inr = true;
+#pragma unroll
+            for (int q = 0; q < kGroupWs; ++q) {
+                if (sizeof(KeyT) == 4)
+                    inr &= ((float)xc[q] >= p.lo_tf) & ((float)xc[q] <= p.hi_tf);
+                else
+                    inr &= ((double)xc[q] >= p.lo_d) & ((double)xc[q] <= p.hi_d);
+            }
+            if (!__all_sync(0xffffffffu, inr)) {
+#pragma unroll
+                for (int q = 0; q < kGroupWs; ++q) {
+                    const uint32_t e = tid + kPredThreads * (g * kGroupWs + q);
+                    KeyT x = xc[q];
+                    if (!KeyTraits<KeyT>::finite(x)) {
+                        atomicMin(&st->bad_index, (unsigned long long)(base + e));
+                        x = (KeyT)p.lo_d;
+                    }
+                    if (e < cnt) {
+                        if (sizeof(KeyT) == 4) {
+                            tail_lo += (float)x < p.lo_tf;
+                            tail_hi += (float)x > p.hi_tf;
+                        } else {
+                            tail_lo += (double)x < p.lo_d;
+                            tail_hi += (double)x > p.hi_d;
+                        }
+                    }
+                    xc[q] = x;
+                }
+            }
             float u[kGroupWs], ul[kGroupWs];
             int32_t y[kGroupWs];
 #pragma unroll
-            for (int q = 0; q < kGroupWs; ++q) {
-                const uint32_t e = tid + kPredThreads * (g * kGroupWs + q);
-                KeyT x = xc[q];
-                if (!KeyTraits<KeyT>::finite(x)) {
-                    atomicMin(&st->bad_index, (unsigned long long)(base + e));
-                    x = (KeyT)p.lo_d;
-                }
-                if (e < cnt) {
-                    if (sizeof(KeyT) == 4) {
-                        tail_lo += (float)x < p.lo_tf;
-                        tail_hi += (float)x > p.hi_tf;
-                    } else {
-                        tail_lo += (double)x < p.lo_d;
-                        tail_hi += (double)x > p.hi_d;
-                    }
-                }
-                key_to_u<KeyT>(x, p, u[q], ul[q]);
-            }
-            // warp-uniform choice: the clamp-free predictor when every key of the warp is inside
-            // the safe range (all keys but far tails)
-            bool safe = true;
+            for (int q = 0; q < kGroupWs; ++q) key_to_u<KeyT>(xc[q], p, u[q], ul[q]);
+            // overflow guard: the per-pair clamp when the weights admit it (packed predictor),
+            // else a warp-uniform choice of the clamp-free chain when every key of the warp is
+            // inside the safe range, and the per-activation clamp otherwise
+            if (PRED == kPredPacked && fw.pair_clamp) {
+                gvm_forward_fxp<MPAD, PRED, kGroupWs, kClampPair>(fw, u, ul, y);
+            } else {
+                bool safe = true;
 #pragma unroll
-            for (int q = 0; q < kGroupWs; ++q) safe &= (u[q] >= fw.u_safe_lo) & (u[q] <= fw.u_safe_hi);
-            if (__all_sync(0xffffffffu, safe))
-                gvm_forward_fxp<MPAD, PRED, kGroupWs, false>(fw, u, ul, y);
-            else
-                gvm_forward_fxp<MPAD, PRED, kGroupWs, true>(fw, u, ul, y);
+                for (int q = 0; q < kGroupWs; ++q) safe &= (u[q] >= fw.u_safe_lo) & (u[q] <= fw.u_safe_hi);
+                if (__all_sync(0xffffffffu, safe))
+                    gvm_forward_fxp<MPAD, PRED, kGroupWs, kClampNone>(fw, u, ul, y);
+                else
+                    gvm_forward_fxp<MPAD, PRED, kGroupWs, kClampAct>(fw, u, ul, y);
+            }
             uint32_t* sbb = sb + buf * T;
 #pragma unroll
-            for (int q = 0; q < kGroupWs; ++q) {
-                const uint32_t e = tid + kPredThreads * (g * kGroupWs + q);
-                const uint32_t b = bucket_of_fxp(y[q], p.bm);
-                sbb[e] = b;
-                if (kPH && e < cnt) {
-                    const uint32_t c = b >> p.fine_bits;
-                    atomicAdd(&hp[buf * hpw + (c >> 1)], 1u << ((c & 1u) << 4));
-                }
-            }
+            for (int q = 0; q < kGroupWs; ++q) sbb[tid + kPredThreads * (g * kGroupWs + q)] = bucket_of_fxp(y[q], p.bm);
             if (g == G - 1) nbar_arrive(kFull0 + buf, kWsThreads);        // sb[buf] is ready
         }
         tail_lo = __reduce_add_sync(0xffffffffu, tail_lo);
@@ -375,60 +373,66 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
         const uint32_t cnt = (uint32_t)min((uint64_t)T, p.n - base);
         const int buf = k & 1;
         const uint32_t* sbb = sb + buf * T;
-        if (!kPH)
-            for (uint32_t c = pt; c < k1ws_c2(C); c += kPartThreads) hist[c] = 0u;
+        for (uint32_t c = pt; c < k1ws_c2(C); c += kPartThreads) hist[c] = 0u;
         nbar_sync(kFull0 + buf, kWsThreads);           // predictors finished tile k (also orders the zeroing)
         if (!PARTITION) {
             if (k + 2 < my_tiles) nbar_arrive(kEmpty0 + buf, kWsThreads);
             continue;
         }
-        // ---- coarse histogram (plain path: already built by the predictor warps in hp[buf])
-        if (!kPH) {
+        // ---- coarse histogram
 #pragma unroll 4
-            for (uint32_t e = pt; e < cnt; e += kPartThreads) atomicAdd(&hist[sbb[e] >> fbits], 1u);
-            nbar_sync(kPart, kPartThreads);
-        }
-        // ---- scan (warp rows, conflict-free) + reservation of this tile's piece in every region.
-        // gbase[c] = region slot of the tile's staged position 0 for coarse bucket c, so a staged
-        // element at position pos goes to gbase[c] + pos.  Regions start at c * capc, or at
-        // rbase[c] (sampled sizes, K0, or exact ones: the retry after an overflow).  A piece that would overflow
-        // its region is marked kOverflowBase and not stored; the call then retries with exact
-        // regions from the final cursors.
+        for (uint32_t e = pt; e < cnt; e += kPartThreads) atomicAdd(&hist[sbb[e] >> fbits], 1u);
+        nbar_sync(kPart, kPartThreads);
+        // ---- scan + reservation of this tile's piece in every region.  gbase[c] = region slot of
+        // the tile's staged position 0 for coarse bucket c, plus T, so a staged element at position
+        // pos goes to gbase[c] + pos - T.  Regions start at c * capc, or at rbase[c] (sampled sizes,
+        // K0, or exact ones: the retry after an overflow).  A piece that would overflow its region
+        // is marked kOverflowBase and not stored; the call then retries with exact regions from the
+        // final cursors.  Each lane takes 4 consecutive counters (128-bit shared loads and stores,
+        // conflict-free), so a warp row covers 128 coarse buckets; counters are zeroed up to
+        // k1ws_c2(C), a multiple of 4.
         {
-            // (even chunks: a u16 counter pair of hp never straddles two warps)
-            const uint32_t chunk = (((C + kPartWarps - 1) / kPartWarps) + 1u) & ~1u;
-            const uint32_t b0 = min(C, (uint32_t)pw * chunk), b1 = min(C, b0 + chunk);
+            const uint32_t C4 = k1ws_c2(C);
+            const uint32_t chunk = ((C4 / 4u + kPartWarps - 1u) / kPartWarps) * 4u;
+            const uint32_t b0 = min(C4, (uint32_t)pw * chunk), b1 = min(C4, b0 + chunk);
             uint32_t carry = 0;
-#pragma unroll 4
-            for (uint32_t r = b0; r < b1; r += 32) {
-                const uint32_t c = r + lane;
-                uint32_t v;
-                if (kPH) {                                     // read and clear the predictor's counters
-                    uint32_t* hw = &hp[buf * hpw + (c >> 1)];
-                    const uint32_t wv = c < b1 ? *hw : 0u;
-                    v = (wv >> ((c & 1u) << 4)) & 0xffffu;
-                    __syncwarp();
-                    if (c < b1 && !(c & 1u)) *hw = 0u;
-                } else {
-                    v = c < b1 ? hist[c] : 0u;
-                }
-                const uint32_t g = v ? atomicAdd(&cursor[c], v) : 0u;
-                uint32_t x = v;
+#pragma unroll 2
+            for (uint32_t r = b0; r < b1; r += 128u) {
+                const uint32_t c0 = r + 4u * (uint32_t)lane;
+                const bool in = c0 < b1;
+                const uint4 v4 = in ? *reinterpret_cast<const uint4*>(hist + c0) : make_uint4(0u, 0u, 0u, 0u);
+                const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
+                uint32_t g[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) g[h] = vv[h] ? atomicAdd(&cursor[c0 + h], vv[h]) : 0u;   // (pads are 0)
+                const uint32_t s4 = vv[0] + vv[1] + vv[2] + vv[3];
+                uint32_t x = s4;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const uint32_t yy = __shfl_up_sync(0xffffffffu, x, o);
                     if (lane >= o) x += yy;
                 }
-                const uint32_t ex = carry + x - v;             // exclusive within the warp's chunk
-                if (c < b1) {
-                    hist[c] = ex;
-                    // region capacity: capc (fixed layout) or rbase[c+1] - rbase[c] (sampled /
-                    // exact layouts, K0 / the retry)
-                    const unsigned long long rcap = rbase ? rbase[c + 1] - rbase[c] : (unsigned long long)p.capc;
-                    const bool fits = (unsigned long long)g + v <= rcap;
-                    over |= !fits;
-                    const long long rb = rbase ? (long long)rbase[c] : (long long)c * p.capc;
-                    gbase[c] = fits ? (uint32_t)(rb + (long long)g + (long long)T - (long long)ex) : kOverflowBase;
+                if (in) {
+                    uint32_t ex = carry + x - s4;              // exclusive within the warp's chunk
+                    uint32_t exs[4], gbs[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const uint32_t c = c0 + h;
+                        exs[h] = ex;
+                        gbs[h] = kOverflowBase;
+                        if (c < C) {
+                            // region capacity: capc (fixed layout) or rbase[c+1] - rbase[c]
+                            // (sampled / exact layouts, K0 / the retry)
+                            const unsigned long long rcap = rbase ? rbase[c + 1] - rbase[c] : (unsigned long long)p.capc;
+                            const bool fits = (unsigned long long)g[h] + vv[h] <= rcap;
+                            over |= !fits;
+                            const long long rb = rbase ? (long long)rbase[c] : (long long)c * p.capc;
+                            if (fits) gbs[h] = (uint32_t)(rb + (long long)g[h] + (long long)T - (long long)ex);
+                        }
+                        ex += vv[h];
+                    }
+                    *reinterpret_cast<uint4*>(hist + c0) = make_uint4(exs[0], exs[1], exs[2], exs[3]);
+                    *reinterpret_cast<uint4*>(gbase + c0) = make_uint4(gbs[0], gbs[1], gbs[2], gbs[3]);
                 }
                 carry += __shfl_sync(0xffffffffu, x, 31);
             }
@@ -443,27 +447,45 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
                 }
         }
         nbar_sync(kPart, kPartThreads);
-        // ---- stage the tile partitioned by coarse id (position -> original offset e, key)
+        // ---- stage the tile partitioned by coarse id (position -> original offset e, key), then
+        // store every piece into its coarse bucket's region (32-bit region slots; an overflowed
+        // piece, gbase = kOverflowBase, is skipped by predication)
+        auto stage_store = [&](auto staged_c) {
+            constexpr bool kStaged = decltype(staged_c)::value;
 #pragma unroll 4
-        for (uint32_t e = pt; e < cnt; e += kPartThreads) {
-            const uint32_t pos = atomicAdd(&hist[sbb[e] >> fbits], 1u);
-            stage_e[pos] = (uint16_t)e;
-            if (staged) stage_key[pos] = keys[base + e];       // L2-resident re-read
-        }
-        nbar_sync(kPart, kPartThreads);
-        // ---- store every piece into its coarse bucket's region
-#pragma unroll 4
-        for (uint32_t pos = pt; pos < cnt; pos += kPartThreads) {
-            const uint32_t e = stage_e[pos];
-            const uint32_t b = sbb[e];
-            const uint32_t gb = gbase[b >> fbits];
-            if (gb != kOverflowBase) {
-                const size_t dst = (size_t)gb + pos - T;
-                reg_keys[dst] = staged ? stage_key[pos] : keys[base + e];
-                reg_fine[dst] = (uint16_t)(b & fmask);
-                if (PERM) reg_idx[dst] = (uint32_t)(base + e);
+            for (uint32_t e = pt; e < cnt; e += kPartThreads) {
+                const uint32_t pos = atomicAdd(&hist[sbb[e] >> fbits], 1u);
+                stage_e[pos] = (uint16_t)e;
+                if (kStaged) stage_key[pos] = keys[base + e];   // L2-resident re-read
             }
-        }
+            nbar_sync(kPart, kPartThreads);
+            KeyT* rk = reg_keys - T;                            // gbase[c] carries + T
+            uint16_t* rf = reg_fine - T;
+            uint32_t* ri = PERM ? reg_idx - T : nullptr;
+            const KeyT* kb = keys + base;
+#pragma unroll 4
+            for (uint32_t pos = pt; pos < cnt; pos += kPartThreads) {
+                const uint32_t e = stage_e[pos];
+                const uint32_t b = sbb[e];
+                const uint32_t gb = gbase[b >> fbits];
+                const KeyT kv = kStaged ? stage_key[pos] : kb[e];
+                const bool ok = gb != kOverflowBase;
+                const uint32_t dst = gb + pos;
+                if (__all_sync(__activemask(), ok)) {          // (overflowed pieces are rare)
+                    rk[dst] = kv;
+                    rf[dst] = (uint16_t)(b & fmask);
+                    if (PERM) ri[dst] = (uint32_t)(base + e);
+                } else if (ok) {
+                    rk[dst] = kv;
+                    rf[dst] = (uint16_t)(b & fmask);
+                    if (PERM) ri[dst] = (uint32_t)(base + e);
+                }
+            }
+        };
+        if (staged)
+            stage_store(std::true_type{});
+        else
+            stage_store(std::false_type{});
         if (k + 2 < my_tiles) nbar_arrive(kEmpty0 + buf, kWsThreads);   // sb[buf] may be refilled
         nbar_sync(kPart, kPartThreads);                // stage_* / hist free for the next tile
     }

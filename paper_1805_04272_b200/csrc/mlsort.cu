@@ -161,7 +161,21 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
         const double C = w.beta[j] * (w.w1[j] + w.b[j]) * log2e + A * (x0 - w.lo);
         return A != 0.0 ? -C / A : 0.0;
     };
-    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return centre(a) < centre(b); });
+    // Models whose neurons all have A_j < 0 (every monotone increasing net the trainer emits) are
+    // ordered by the left saturation bound instead (a_j = 24.5), which pairs neurons whose
+    // per-pair clamp interval is non-empty (predict.cuh FoldedWeights::Lp; checked below).
+    auto coefA = [&](uint32_t j) { return -2.0 * w.beta[j] * w.w1[j] * log2e / span; };
+    bool all_neg = w.m > 0;
+    for (uint32_t j = 0; j < w.m; ++j) all_neg &= coefA(j) < 0.0;
+    auto left_bound = [&](uint32_t j) {
+        const double A = coefA(j);
+        const double C = w.beta[j] * (w.w1[j] + w.b[j]) * log2e + A * (x0 - w.lo);
+        return (24.5 - C) / A;
+    };
+    if (all_neg && !std::getenv("MLSORT_NO_PAIR_CLAMP"))
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return left_bound(a) < left_bound(b); });
+    else
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return centre(a) < centre(b); });
     for (uint32_t j = 0; j < mpad; ++j) {
         if (j < w.m) {
             const uint32_t o = order[j];
@@ -291,6 +305,32 @@ FoldedWeights fold(const Weights& w, uint32_t mpad, bool f32) {
             f.u_safe_lo = -INFINITY;
             f.u_safe_hi = INFINITY;
         }
+    }
+    // ---- per-pair lower clamp (predict.cuh FoldedWeights::Lp): for u >= L_p every argument of
+    // the pair is <= 119 (the chain's d stays <= 2^120), and L_p lies below both neurons' left
+    // saturation bound (a >= 24.5: the computed term is the exact constant 0, as for every u < L_p),
+    // so max(u, L_p) changes no output bit.  Pad neurons (A = 0, a = 0) accept any L_p.
+    f.pair_clamp = 0;
+    if (all_neg && !std::getenv("MLSORT_NO_PAIR_CLAMP")) {
+        bool ok = true;
+        for (uint32_t pp = 0; pp < mpad / 2 && ok; ++pp) {
+            double thr = -INFINITY, lob = INFINITY;
+            for (uint32_t h = 0; h < 2; ++h) {
+                const uint32_t j = 2 * pp + h;
+                const double A = f.A[j], C = f.Cs[j];
+                if (A < 0.0) {
+                    thr = std::max(thr, ((double)kANoClamp - 1.0 - C) / A);
+                    lob = std::min(lob, (24.5 - C) / A);
+                } else if (A > 0.0 || C > (double)kANoClamp - 1.0) {
+                    ok = false;
+                }
+            }
+            float L = thr == -INFINITY ? -INFINITY : (float)thr;
+            if (std::isfinite(L) && (double)L < thr) L = std::nextafter(L, INFINITY);   // round up
+            ok = ok && (double)L <= lob - 1e-6 * std::max(1.0, std::fabs(lob));
+            f.Lp[pp] = L;
+        }
+        f.pair_clamp = ok ? 1u : 0u;
     }
     auto pair = [](float v) {
         uint32_t bb;
@@ -1470,7 +1510,7 @@ k_predict(const KeyT* __restrict__ keys, uint64_t n, FoldedWeights fw, K1Params 
             const float umax = __uint_as_float((omx & 0x80000000u) ? (omx & 0x7fffffffu) : ~omx);
             gvm_forward_skip<MPAD, G, true>(fw, u, umin, umax, y);
         } else {
-            gvm_forward_fxp<MPAD, PRED, G>(fw, u, ul, y);
+            gvm_forward_dense<MPAD, PRED, G>(fw, u, ul, y);
         }
 #pragma unroll
         for (int q = 0; q < G; ++q) {

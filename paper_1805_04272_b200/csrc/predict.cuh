@@ -31,6 +31,15 @@ struct __align__(16) FoldedWeights {
     // packed predictor, exponent-shifted (see kAShift): Cs_j = C_j - kAShift, Wns_j = -W_j 2^-kAShift
     float Cs[kMaxM];
     float Wns[kMaxM];
+    // Per-pair lower clamp of the packed predictor (pair_clamp != 0; DESIGN.md "K1 per-pair
+    // clamp"): for models whose neurons all have A_j < 0 the host orders the neurons by their left
+    // saturation bound and checks, for every pair p, that L_p = max_j (119 - Cs_j)/A_j (every
+    // argument <= 119 for u >= L_p) lies below both neurons' left saturation bound (a_j >= 24.5,
+    // where the computed term is the exact constant 0).  Then u_p = max(u, L_p) changes no term
+    // and no argument can overflow the reciprocal chain: one FMNMX per pair and key instead of one
+    // per activation.
+    float Lp[kMaxM / 2];
+    uint32_t pair_clamp;
     // u in [u_safe_lo, u_safe_hi] keeps every shifted argument A_j u + Cs_j <= kAClamp, so the
     // packed predictor may skip its per-activation clamp for such keys (CLAMP = false).  When
     // u_cl_lo/hi are finite, keys clamp u into [u_cl_lo, u_cl_hi] (K1Params), every argument
@@ -172,9 +181,13 @@ constexpr int32_t kFxpMagicBits = 0x4B400000;
 // MPAD is the padded neuron count (pad neurons have W = 0).  PRED selects the reciprocal
 // formulation; in kPredMixed one neuron in four uses MUFU.RCP and three use the Newton
 // reciprocal, balancing MUFU (ex2) load against FMA-pipe issue.
-// CLAMP = false is valid only when every key of the group has u in [u_safe_lo, u_safe_hi]
-// (then a_j <= 59 for every neuron and d = 1 + 2^a is finite without the clamp).
-template <int MPAD, int PRED, int KG, bool CLAMP = true>
+// Overflow guard of the reciprocal chain (d = 1 + 2^a must stay <= 2^120):
+//   kClampNone: none -- valid only when every key of the group has u in [u_safe_lo, u_safe_hi]
+//               (then a_j <= 59 for every neuron);
+//   kClampAct:  a_j = min(a_j, 60) per activation (any model);
+//   kClampPair: u_p = max(u, Lp[p]) per neuron pair (packed predictor, fw.pair_clamp != 0).
+enum { kClampNone = 0, kClampAct = 1, kClampPair = 2 };
+template <int MPAD, int PRED, int KG, int CLAMP = kClampAct>
 __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const float (&uh)[KG],
                                                 const float (&ul)[KG], int32_t (&acc)[KG]) {
 #pragma unroll
@@ -188,10 +201,11 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
         for (int j = 0; j < MPAD / 2; ++j) {
 #pragma unroll
             for (int q = 0; q < KG; ++q) {
-                const f32x2 a2 = ffma2(pk2(uh[q], uh[q]), A2[j], C2[j]);     // a - s
+                const float up = CLAMP == kClampPair ? fmaxf(uh[q], fw.Lp[j]) : uh[q];
+                const f32x2 a2 = ffma2(pk2(up, up), A2[j], C2[j]);     // a - s
                 float a0, a1;
                 upk2(a2, a0, a1);
-                if (CLAMP) {
+                if (CLAMP == kClampAct) {
                     a0 = fminf(a0, kAClamp);         // d stays finite and normal
                     a1 = fminf(a1, kAClamp);
                 }
@@ -218,7 +232,7 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
                 if (use_mufu_rcp) {
                     r = rcp_approx(1.0f + ex2_approx(a));
                 } else {
-                    a = fminf(a, 60.0f);             // keeps d = 1 + 2^a inside Newton's range
+                    a = fminf(a, 60.0f);             // keeps d = 1 + 2^a inside Newton's range (any CLAMP)
                     r = rcp_newton(1.0f + ex2_approx(a));
                 }
                 t[h][q] = __float_as_int(fmaf(r, W, kFxpMagic));
@@ -228,6 +242,18 @@ __device__ __forceinline__ void gvm_forward_fxp(const FoldedWeights& fw, const f
         for (int q = 0; q < KG; ++q) acc[q] = (int32_t)((uint32_t)acc[q] + (uint32_t)t[0][q] + (uint32_t)t[1][q]);
     }
     }
+}
+
+// The dense evaluation every kernel outside k1_ws's per-warp choice uses: the per-pair clamp when
+// the host established it for these weights (packed predictor), else the per-activation clamp.
+// For keys the clamps do not move, both give the bits of the clamp-free chain.
+template <int MPAD, int PRED, int KG>
+__device__ __forceinline__ void gvm_forward_dense(const FoldedWeights& fw, const float (&uh)[KG],
+                                                  const float (&ul)[KG], int32_t (&acc)[KG]) {
+    if (PRED == kPredPacked && fw.pair_clamp)
+        gvm_forward_fxp<MPAD, PRED, KG, kClampPair>(fw, uh, ul, acc);
+    else
+        gvm_forward_fxp<MPAD, PRED, KG, kClampAct>(fw, uh, ul, acc);
 }
 
 // Packed predictor with saturated-pair skipping for a group of KG keys per lane whose u lie in

@@ -413,3 +413,41 @@ def test_key_clamp_bit_identical(mls, name, pred):
         y0, b0 = mls.predict(_t(keys), w_ref, num_buckets=B, predictor=pred)
         assert bool((y1.view(torch_int32()) == y0.view(torch_int32())).all())
         assert bool((b1 == b0).all())
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C4", "C5"])
+def test_pair_clamp_bit_identical(mls, name):
+    """The per-pair lower clamp of the packed predictor (FoldedWeights::Lp; DESIGN.md "K1 per-pair
+    clamp") replaces the per-activation clamp: for u below L_p both neurons of the pair are in
+    their left saturation (exact constant terms) and above it no argument overflows, so no output
+    bit changes.  Compared against the same weights folded with MLSORT_NO_PAIR_CLAMP=1 (the
+    per-activation clamp), on keys spanning the whole finite range plus the config's own keys,
+    through mlsort_predict (y and b) and through the sort (k1_ws's clamp choice)."""
+    import os
+    cfg = workloads.CONFIGS[name]
+    p = workloads.load_weights_dict(name)
+    w = mls.Weights.from_dict(p)
+    os.environ["MLSORT_NO_PAIR_CLAMP"] = "1"
+    try:
+        w_ref = mls.Weights.from_dict(p)
+        mls.predict(_t(np.zeros(8, dtype=np.float32)), w_ref)           # fold now
+    finally:
+        del os.environ["MLSORT_NO_PAIR_CLAMP"]
+    rng = np.random.default_rng(6)
+    big = np.finfo(np.float32).max
+    wide = np.sign(rng.random(1 << 18) - 0.5) * np.exp(rng.uniform(-80, np.log(big), 1 << 18))
+    keys = np.concatenate([workloads.generate_config(cfg, n=1 << 18), wide.astype(np.float32),
+                           np.array([p["input_lo"], p["input_hi"], -big, big, 0.0], dtype=np.float32)])
+    for B in (cfg.buckets, 1000):
+        y1, b1 = mls.predict(_t(keys), w, num_buckets=B)
+        y0, b0 = mls.predict(_t(keys), w_ref, num_buckets=B)
+        assert bool((y1.view(torch_int32()) == y0.view(torch_int32())).all())
+        assert bool((b1 == b0).all())
+    n = 1 << 20
+    k2 = workloads.generate_config(cfg, n=n)
+    k, pm, info = mls.sort(_t(k2), w, perm=cfg.perm, num_buckets=min(cfg.buckets, n))
+    ref_keys, ref_perm = oracle.sorted_reference(k2)
+    np.testing.assert_array_equal(_bits(k.cpu().numpy()), _bits(ref_keys))
+    if cfg.perm:
+        np.testing.assert_array_equal(pm.cpu().numpy().astype(np.uint32), ref_perm)
+    assert info["repairs"] == 0 and info["fallback_used"] == 0, info
