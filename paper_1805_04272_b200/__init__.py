@@ -261,6 +261,8 @@ class Sorter:
         self.ws_bytes = workspace_size(n, self.dt, perm, num_buckets, predictor)
         self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=self.device)
         self.last_info = Info()
+        self._opts = _opts(self.num_buckets, self.predictor, self.timing)     # built once
+        self._fn = lib().mlsort_sort
 
     def __call__(self, keys, out_keys=None, out_perm=None, payload=None, out_payload=None, stream=None):
         torch = _torch()
@@ -275,14 +277,13 @@ class Sorter:
             out_perm = torch.empty(n, dtype=torch.int32, device=keys.device)
         if payload is not None and out_payload is None:
             out_payload = torch.empty(n, dtype=torch.int32, device=keys.device)
-        o = _opts(self.num_buckets, self.predictor, self.timing)
         info = Info()
-        rc = lib().mlsort_sort(C.c_void_p(keys.data_ptr()),
-                               C.c_void_p(payload.data_ptr()) if payload is not None else None, n, self.dt,
-                               self._w.handle, C.byref(o), C.c_void_p(out_keys.data_ptr()),
-                               C.c_void_p(out_perm.data_ptr()) if self.perm else None,
-                               C.c_void_p(out_payload.data_ptr()) if payload is not None else None,
-                               C.c_void_p(self.ws.data_ptr()), self.ws_bytes, _stream_ptr(stream), C.byref(info))
+        rc = self._fn(keys.data_ptr(), payload.data_ptr() if payload is not None else None, n, self.dt,
+                      self._w.handle, C.byref(self._opts), out_keys.data_ptr(),
+                      out_perm.data_ptr() if self.perm else None,
+                      out_payload.data_ptr() if payload is not None else None,
+                      self.ws.data_ptr(), self.ws_bytes,
+                      (stream if stream is not None else torch.cuda.current_stream()).cuda_stream, C.byref(info))
         self.last_info = info
         _check(rc, "mlsort_sort", info)
         return out_keys, out_perm, out_payload, info
