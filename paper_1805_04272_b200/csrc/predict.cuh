@@ -312,10 +312,16 @@ __device__ __forceinline__ uint32_t f32_ordbits(float x) {
 // (S:232, S:297-S:298).  For y >= 0 round-half-up equals round-half-away-
 // from-zero (reading A6); negative y map to bucket 0.
 __device__ __forceinline__ uint32_t bucket_of_fxp(int32_t acc, const BucketMap& bm) {
+    if (bm.pow2 && bm.sh >= 0) {
+        // B = 2^k, sh = S - k >= 0: (acc * 2^k + 2^(S-1)) >> S == (acc + 2^(sh-1)) >> sh (half = 0
+        // for sh = 0), exactly, in 32-bit arithmetic: |acc| < M * 2^22 <= 2^28 (fxp_shift), so
+        // acc + half cannot overflow; the arithmetic shift keeps negative sums negative
+        const int32_t r = (acc + bm.half) >> bm.sh;
+        return (uint32_t)min(max(r, 0), (int32_t)bm.Bm1);
+    }
     if (bm.pow2) {
-        // B = 2^k: (acc * 2^k + 2^(S-1)) >> S == (acc + 2^(sh-1)) >> sh for sh = S - k > 0,
-        // == acc for sh = 0 and == acc * 2^-sh for sh < 0 (the 1/2 floors away), exactly
-        long long r = bm.sh >= 0 ? (long long)((acc + bm.half) >> bm.sh) : (long long)acc << (-bm.sh);
+        // sh < 0: acc * 2^-sh (the 1/2 floors away), exactly
+        long long r = (long long)acc << (-bm.sh);
         r = r < 0 ? 0 : r;
         return r < (long long)bm.Bm1 ? (uint32_t)r : bm.Bm1;
     }
