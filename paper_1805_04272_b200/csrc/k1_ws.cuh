@@ -29,6 +29,10 @@ namespace mlsort {
 #ifndef MLSORT_K1_PREDW
 #define MLSORT_K1_PREDW 24
 #endif
+#ifndef MLSORT_K1_SETMAXNREG
+#define MLSORT_K1_SETMAXNREG 0  // 1: plain path moves registers from the partition warps (40) to the
+                                // predictor warps (72) with setmaxnreg (launched at 64 each)
+#endif
 #ifndef MLSORT_K1_GROUP24
 #define MLSORT_K1_GROUP24 1    // grouped variant: 24 predictor warps, u re-read from the keys (0: 16 warps, u in smem)
 #endif
@@ -268,6 +272,8 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
 
     if (warp < kPredWarps) {
         // ===================================================== predictor warps
+        if (MLSORT_K1_SETMAXNREG && kPredWarps % 4 == 0 && kPartWarps % 4 == 0)
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 72;\n" ::: "memory");
         // The (tile, group) sequence is flattened so the keys of the next group -- possibly
         // the first group of the next tile -- are loaded while the current group is evaluated.
         constexpr int G = KPT / kGroupWs;                  // groups per tile
@@ -362,6 +368,8 @@ k1_ws(const KeyT* __restrict__ keys, K1Params p, KeyT* __restrict__ reg_keys,
     }
 
     // ===================================================== partition warps
+    if (MLSORT_K1_SETMAXNREG && !GROUP && kPredWarps % 4 == 0 && kPartWarps % 4 == 0)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     const int pt = tid - kPredThreads;                 // 0 .. kPartThreads-1
     const int pw = warp - kPredWarps;
     const uint32_t fbits = p.fine_bits;

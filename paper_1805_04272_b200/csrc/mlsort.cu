@@ -444,16 +444,18 @@ Plan make_plan(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws = tru
     p.sampled = allow_ws && n >= kSampledMinN && !std::getenv("MLSORT_NO_SAMPLE");
     p.stride = std::max<uint64_t>(1, n / kSampleTarget);
     set_region_area(p);
-    if (allow_ws) {
-        const uint32_t wt = ws_tile_of(ks, group);
-        size_t sm = k1ws_smem_bytes(ks, wt, p.C, group, true);
+    // the value-grouped variant when asked for and its shared memory fits, else the plain one
+    for (int gi = group ? 0 : 1; allow_ws && gi < 2 && !p.ws; ++gi) {
+        const bool g = gi == 0;
+        const uint32_t wt = ws_tile_of(ks, g);
+        size_t sm = k1ws_smem_bytes(ks, wt, p.C, g, true);
         p.ws_stage = sm <= kK1WsSmemMax && !std::getenv("MLSORT_NO_STAGE");
-        if (!p.ws_stage) sm = k1ws_smem_bytes(ks, wt, p.C, group, false);
+        if (!p.ws_stage) sm = k1ws_smem_bytes(ks, wt, p.C, g, false);
         // k1_ws keeps 32-bit region slots (+ tile) with 0xFFFFFFFF reserved
         const bool slots32 = p.area + p.tile + (uint64_t)wt + 8 < 0xFFFFFFFFull;
         if (sm <= kK1WsSmemMax && slots32) {
             p.ws = true;
-            p.ws_group = group;
+            p.ws_group = g;
             p.tile = wt;
             p.T = (uint32_t)((n + wt - 1) / wt);
             p.k1_smem = sm;
@@ -506,6 +508,10 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
         p.k1_smem = k1;
         p.k3_smem = k3l_smem_bytes(ks, perm, kfine, (uint32_t)cap, kL3ThreadsBig);
         // two-CTA primary pass only when it holds the average bucket with margin
+        // (the primary pass keeps kfine counters although it merges rank-bucket pairs: sizing it
+        // for the merged buckets -- cap1 18432 -> 22528 on C2 -- moved buckets from the
+        // 1024-thread secondary pass into it and made K3 slower, 0.389 -> 0.396 ms,
+        // profiles/r02/ab_k3_cap1_finebits13_rejected.log)
         p.cap1 = k3l_cap_for(kK3LSmemPrimary, ks, perm, kfine, kL3Threads);
         if ((double)p.cap1 < 1.1 * avg + 64.0) p.cap1 = 0;
         p.k3_smem1 = p.cap1 ? k3l_smem_bytes(ks, perm, kfine, p.cap1, kL3Threads) : 0;
@@ -1221,6 +1227,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
             if (off <= p.area) {
                 unsigned long long* d_rb = at<unsigned long long>(ws, L.rbase);
                 CK(cudaMemcpyAsync(d_rb, rb.data(), (size_t)(p.C + 1) * 8, cudaMemcpyHostToDevice, s));
+                CK(cudaStreamSynchronize(s));          // (the host vectors die at scope end)
                 rbase = d_rb;
                 continue;
             }
