@@ -238,9 +238,16 @@ k0_init(DevStatus* __restrict__ st, unsigned long long* __restrict__ range_start
 
 static __global__ void __launch_bounds__(1024)
 k2_coarse_starts(const uint32_t* __restrict__ cursor, uint32_t C, unsigned long long* __restrict__ starts,
-                 bool one_pass) {
+                 bool one_pass, uint32_t mid_cap = 0, uint32_t* __restrict__ mid_list = nullptr,
+                 DevStatus* __restrict__ st = nullptr) {
     __shared__ uint32_t scratch[64];
     __shared__ unsigned long long carry;
+    // coarse buckets larger than the K3 primary pass holds (mid_cap > 0): listed here, so the
+    // secondary pass can run concurrently with the primary one instead of after it
+    if (mid_cap) {
+        for (uint32_t c = threadIdx.x; c < C; c += 1024u)
+            if (cursor[c] > mid_cap) mid_list[atomicAdd(&st->mid_count, 1ull)] = c;
+    }
     const uint32_t k = (C + 1023u) / 1024u;              // counts per thread
     if (one_pass && k <= 16u) {                          // (one_pass: the total fits 32 bits)
         // one pass: every thread loads its k consecutive counts at once (one memory latency),

@@ -359,4 +359,26 @@ __global__ void k5_item_verify(const K3Item* __restrict__ items, const K3Seg* __
     }
 }
 
+// K5 in one launch: every recorded coarse-bucket / K4-run start (range_start, the work of
+// k5_boundary_verify) and every item / segment start (k5_item_verify), grid-stride.
+template <typename KeyT, bool PERM>
+__global__ void k5_verify_all(const unsigned long long* __restrict__ range_start, uint64_t nranges,
+                              const K3Item* __restrict__ items, const K3Seg* __restrict__ segs,
+                              const KeyT* __restrict__ out_keys, const uint32_t* __restrict__ out_perm,
+                              DevStatus* __restrict__ st, uint32_t item_cap, uint32_t seg_cap, uint64_t n) {
+    const uint64_t ni = min((unsigned long long)item_cap, st->item_count);
+    const uint64_t ns = min((unsigned long long)seg_cap, st->seg_count);
+    bool bad = false;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nranges + ni + ns;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long s = i < nranges ? range_start[i]
+                                     : (i < nranges + ni ? items[i - nranges].out : segs[i - nranges - ni].out);
+        if (s == ~0ull || s == 0 || s >= n) continue;
+        const auto a = KeyTraits<KeyT>::to_ord(out_keys[s - 1]);
+        const auto b = KeyTraits<KeyT>::to_ord(out_keys[s]);
+        bad |= PERM ? !(a < b || (a == b && out_perm[s - 1] < out_perm[s])) : (b < a);
+    }
+    if (bad) atomicAdd(&st->violations, 1ull);
+}
+
 }  // namespace mlsort

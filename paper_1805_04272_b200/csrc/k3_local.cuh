@@ -64,6 +64,7 @@ struct K3LParams {
                             // K4's big_list (0)
     uint32_t item_cap;      // ITEMS pass: capacity of the item list (k3_big.cuh)
     uint32_t fshift;        // coarse-bucket passes: rank bucket = fine id >> fshift (experiments)
+    uint32_t premid;        // primary pass: K2 already listed the too-large buckets (skip them)
 };
 
 // The rank-bucket histogram holds two u16 counters per 32-bit word (a coarse bucket never
@@ -440,7 +441,9 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             }
             if (tid == 0) {
                 atomicMax(&st->max_coarse, (unsigned long long)n);
-                if (p.to_mid) {
+                if (p.premid) {
+                    // (K2 listed it for the concurrent secondary pass)
+                } else if (p.to_mid) {
                     mid_list[atomicAdd(&st->mid_count, 1ull)] = c;
                 } else if (atomicExch(&big_mark[c], 1u) == 0u) {
                     const unsigned long long k = atomicAdd(&st->big_count, 1ull);

@@ -513,7 +513,7 @@ Plan make_plan_base(uint64_t n, uint64_t B, size_t ks, bool perm, bool allow_ws)
         // 1024-thread secondary pass into it and made K3 slower, 0.389 -> 0.396 ms,
         // profiles/r02/ab_k3_cap1_finebits13_rejected.log)
         p.cap1 = k3l_cap_for(kK3LSmemPrimary, ks, perm, kfine, kL3Threads);
-        if ((double)p.cap1 < 1.1 * avg + 64.0) p.cap1 = 0;
+        if ((double)p.cap1 < 1.1 * avg + 64.0 || std::getenv("MLSORT_K3_NO_PRIMARY")) p.cap1 = 0;
         p.k3_smem1 = p.cap1 ? k3l_smem_bytes(ks, perm, kfine, p.cap1, kL3Threads) : 0;
         uint64_t cc = (uint64_t)std::ceil(kRegionFactor * avg) + 64;
         cc = (cc + 7) & ~7ull;
@@ -709,7 +709,7 @@ cudaError_t launch_k1(const Plan& p, const KeyT* keys, uint32_t mpad, int pred, 
 template <typename KeyT, bool PERM, int NT, bool ITEMS = false>
 cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_keys, uint32_t* out_perm, cudaStream_t s,
                            bool secondary, bool to_mid, uint32_t cap, size_t smem, int grid,
-                           const unsigned long long* rbase) {
+                           const unsigned long long* rbase, bool premid = false) {
     auto kern = k3_local_sort<KeyT, PERM, NT, ITEMS>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
@@ -721,6 +721,7 @@ cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_k
     kp.secondary = secondary ? 1u : 0u;
     kp.to_mid = to_mid ? 1u : 0u;
     kp.item_cap = p.item_cap;
+    kp.premid = premid ? 1u : 0u;
     {   // the coarse-bucket passes merge rank-bucket pairs (fine id >> 1: ~2 keys per rank bucket
         // at B = N): C2 K3 0.416 -> 0.390 ms (>> 2: 0.508, >> 3: 0.731; profiles/r02/k3_fshift.log).
         // MLSORT_K3_FSHIFT=k overrides (experiments).
@@ -775,6 +776,28 @@ cudaError_t launch_k3_big(const Plan& p, void* ws, const Layout& L, KeyT* out_ke
     return e;
 }
 
+// Auxiliary stream and fork/join events of the concurrent K3 passes, per (thread, device).
+struct ForkStreams {
+    int dev = -1;
+    cudaStream_t aux = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+ForkStreams& fork_streams() {
+    thread_local std::vector<ForkStreams> all;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (auto& f : all)
+        if (f.dev == dev) return f;
+    ForkStreams f;
+    f.dev = dev;
+    if (cudaStreamCreateWithFlags(&f.aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming) != cudaSuccess)
+        f.aux = nullptr;
+    all.push_back(f);
+    return all.back();
+}
+
 // K3 local plan: primary pass (two 512-thread CTAs per SM, capacity cap1) over every coarse
 // bucket, then the secondary pass (one 1024-thread CTA per SM, capacity cap) over the buckets
 // the primary pass handed over.
@@ -783,11 +806,26 @@ cudaError_t launch_k3_local(const Plan& p, void* ws, const Layout& L, KeyT* out_
                             cudaStream_t s, const unsigned long long* rbase) {
     cudaError_t e;
     if (p.cap1 > 0) {
-        e = launch_k3_pass<KeyT, PERM, kL3Threads>(p, ws, L, out_keys, out_perm, s, false, true, p.cap1,
-                                                   p.k3_smem1, std::min<int>(2 * num_sms(), (int)p.C), rbase);
+        // K2 listed the coarse buckets above cap1, so the secondary pass (one 1024-thread CTA per
+        // SM) runs on a forked stream concurrently with the primary pass: the large buckets
+        // start first and the primary pass's CTAs fill every SM they free, instead of the
+        // secondary pass running alone after the primary pass's tail
+        ForkStreams& fk = fork_streams();
+        if (!fk.aux) return cudaErrorNotReady;
+        e = cudaEventRecord(fk.fork, s);
         if (e != cudaSuccess) return e;
-        e = launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, true, false,
+        e = cudaStreamWaitEvent(fk.aux, fk.fork, 0);
+        if (e != cudaSuccess) return e;
+        e = launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, fk.aux, true, false,
                                                       p.cap, p.k3_smem, num_sms(), rbase);
+        if (e != cudaSuccess) return e;
+        e = cudaEventRecord(fk.join, fk.aux);
+        if (e != cudaSuccess) return e;
+        e = launch_k3_pass<KeyT, PERM, kL3Threads>(p, ws, L, out_keys, out_perm, s, false, true, p.cap1,
+                                                   p.k3_smem1, std::min<int>(2 * num_sms(), (int)p.C), rbase,
+                                                   true);
+        if (e != cudaSuccess) return e;
+        e = cudaStreamWaitEvent(s, fk.join, 0);
     } else {
         e = launch_k3_pass<KeyT, PERM, kL3ThreadsBig>(p, ws, L, out_keys, out_perm, s, false, false,
                                                       p.cap, p.k3_smem, std::min<int>(num_sms(), (int)p.C), rbase);
@@ -1126,6 +1164,7 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     DevStatus st;
     const unsigned long long* rbase = nullptr;   // regions at c * capc; K0-sized or exact (retry) layouts
     const uint64_t nranges = (uint64_t)p.C * p.R;
+    if (p.local && p.cap1 > 0) fork_streams();       // (created outside any graph capture)
     // One attempt's device work, from the status reset to the status read, enqueued on q (the
     // caller's stream, or the capture stream of the graph path below).
     auto enqueue = [&](cudaStream_t q, int attempt) -> int {
@@ -1159,7 +1198,8 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         }
         tm.mark();
         k2_coarse_starts<<<1, 1024, 0, q>>>(at<uint32_t>(ws, L.cursor), p.C, at<unsigned long long>(ws, L.starts),
-                                            n < (1ull << 31));
+                                            n < (1ull << 31), p.local ? p.cap1 : 0u, at<uint32_t>(ws, L.mid_list),
+                                            dst);
         CK(cudaGetLastError());
         tm.mark();
         // K3 checks the adjacent order of every coarse bucket it sorts (reading A14) for every
@@ -1175,14 +1215,14 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
         }
         tm.mark();
         tm.mark();
-        k5_boundary_verify<KeyT, PERM><<<(unsigned)((nranges + 255) / 256), 256, 0, q>>>(
-            at<unsigned long long>(ws, L.range_start), nranges, out_keys, out_perm, dst);
-        CK(cudaGetLastError());
-        k5_item_verify<KeyT, PERM><<<num_sms() * 2, 256, 0, q>>>(at<K3Item>(ws, L.items), at<K3Seg>(ws, L.k3segs),
-                                                                 out_keys, out_perm, dst, p.item_cap, p.seg_cap, n);
+        k5_verify_all<KeyT, PERM><<<(unsigned)std::max<uint64_t>(num_sms() * 2, std::min<uint64_t>((nranges + 255) / 256,
+                                                                                              num_sms() * 8)),
+                                    256, 0, q>>>(at<unsigned long long>(ws, L.range_start), nranges,
+                                                 at<K3Item>(ws, L.items), at<K3Seg>(ws, L.k3segs), out_keys,
+                                                 out_perm, dst, p.item_cap, p.seg_cap, n);
         CK(cudaGetLastError());
         tm.mark();
-        nl.count += 7 + (p.cap1 > 0 ? 1 : 0) + (PERM ? 1 : 0);
+        nl.count += 6 + (p.cap1 > 0 ? 1 : 0) + (PERM ? 1 : 0);
 
         CK(cudaMemcpyAsync(hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, q));
         return MLSORT_OK;
