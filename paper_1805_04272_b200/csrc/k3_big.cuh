@@ -231,6 +231,25 @@ constexpr uint32_t kIdxSortMax = 1u << 21;
 constexpr uint32_t kIdxSub = 4096;           // max sub-buckets per run
 constexpr uint32_t kIdxWarpBuf = 224;
 
+// Every element of the u32 run v[0, len) once, in 128-bit loads where aligned (scalar head and
+// tail): fn(i, value) for the block's threads.
+template <int NT, typename Fn>
+__device__ __forceinline__ void for_each_u32(const uint32_t* v, uint32_t len, Fn&& fn) {
+    const uint32_t head = min(len, (uint32_t)((16u - ((uint32_t)reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
+    if (threadIdx.x < head) fn(threadIdx.x, v[threadIdx.x]);
+    const uint32_t nv = (len - head) / 4u;
+    const uint4* v4 = reinterpret_cast<const uint4*>(v + head);
+    for (uint32_t k = threadIdx.x; k < nv; k += NT) {
+        const uint4 q = v4[k];
+        const uint32_t i = head + 4u * k;
+        fn(i, q.x);
+        fn(i + 1, q.y);
+        fn(i + 2, q.z);
+        fn(i + 3, q.w);
+    }
+    for (uint32_t i = head + 4u * nv + threadIdx.x; i < len; i += NT) fn(i, v[i]);
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT, NT == 512 ? 3 : 1)
 k3_index_sort(K3Seg* __restrict__ segs, uint32_t seg_cap, uint32_t* __restrict__ perm, uint32_t* __restrict__ tmp,
@@ -256,11 +275,10 @@ k3_index_sort(K3Seg* __restrict__ segs, uint32_t seg_cap, uint32_t* __restrict__
         }
         __syncthreads();
         uint32_t lmin = 0xffffffffu, lmax = 0u;
-        for (uint32_t i = tid; i < len; i += NT) {
-            const uint32_t v = pv[i];
+        for_each_u32<NT>(pv, len, [&](uint32_t, uint32_t v) {
             lmin = min(lmin, v);
             lmax = max(lmax, v);
-        }
+        });
         lmin = __reduce_min_sync(0xffffffffu, lmin);
         lmax = __reduce_max_sync(0xffffffffu, lmax);
         if (lane == 0) {
@@ -275,7 +293,7 @@ k3_index_sort(K3Seg* __restrict__ segs, uint32_t seg_cap, uint32_t* __restrict__
         const uint64_t range = (uint64_t)s_max - vmin + 1;
         uint32_t sh = 0;
         while ((range - 1) >> sh >= nsb) ++sh;
-        for (uint32_t i = tid; i < len; i += NT) atomicAdd(&cnt[(pv[i] - vmin) >> sh], 1u);
+        for_each_u32<NT>(pv, len, [&](uint32_t, uint32_t v) { atomicAdd(&cnt[(v - vmin) >> sh], 1u); });
         __syncthreads();
         if (warp == 0) {                               // exclusive scan of nsb (<= 4096) counts
             const uint32_t per = (nsb + 31) / 32;
@@ -298,10 +316,7 @@ k3_index_sort(K3Seg* __restrict__ segs, uint32_t seg_cap, uint32_t* __restrict__
         }
         __syncthreads();
         // scatter into sub-bucket order; afterwards cnt[j] = end of sub-bucket j
-        for (uint32_t i = tid; i < len; i += NT) {
-            const uint32_t v = pv[i];
-            tv[atomicAdd(&cnt[(v - vmin) >> sh], 1u)] = v;
-        }
+        for_each_u32<NT>(pv, len, [&](uint32_t, uint32_t v) { tv[atomicAdd(&cnt[(v - vmin) >> sh], 1u)] = v; });
         __syncthreads();
         for (uint32_t j = warp; j < nsb; j += NT / 32) {
             const uint32_t b = j ? cnt[j - 1] : 0u, e = cnt[j], sz = e - b;
@@ -331,7 +346,9 @@ k3_index_sort(K3Seg* __restrict__ segs, uint32_t seg_cap, uint32_t* __restrict__
             if (tid == 0) segs[g].pad = 1u;
         } else {
             uint32_t viol = 0;                         // reading A14: strictly ascending indices
-            for (uint32_t i = tid + 1; i < len; i += NT) viol += pv[i - 1] < pv[i] ? 0u : 1u;
+            for_each_u32<NT>(pv, len, [&](uint32_t i, uint32_t v) {
+                if (i) viol += pv[i - 1] < v ? 0u : 1u;     // (the predecessor: L1-resident)
+            });
             viol = __reduce_add_sync(0xffffffffu, viol);
             if (lane == 0 && viol) atomicAdd(&st->violations, (unsigned long long)viol);
             if (tid == 0) segs[g].pad = 0u;
