@@ -17,8 +17,8 @@ CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline $EXTRA"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1; echo ncu_launch=$?
 for K in k1_ws k3_local; do
-  S=3; [ $K = k3_local ] && S=6
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 -o /tmp/${TAG}_$K $CMD > gpurun_out/${TAG}_ncu_$K.log 2>&1; echo ncu_$K=$?
+  S=3; KRE=k1_ws; [ $K = k3_local ] && S=6 && KRE="k3_local_sort<.*512"
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$KRE" -s $S -c 1 -o /tmp/${TAG}_$K $CMD > gpurun_out/${TAG}_ncu_$K.log 2>&1; echo ncu_$K=$?
   ncu -i /tmp/${TAG}_$K.ncu-rep --page raw --csv > gpurun_out/${TAG}_$K.raw.csv 2>&1
   ncu -i /tmp/${TAG}_$K.ncu-rep --page details --csv > gpurun_out/${TAG}_$K.details.csv 2>&1
   ncu -i /tmp/${TAG}_$K.ncu-rep --page source --csv > gpurun_out/${TAG}_$K.source.csv 2>&1
