@@ -31,7 +31,9 @@ struct DevStatus {
     unsigned long long ticket3c;    // k3_cut ticket
     unsigned long long ticket3d;    // K3 round-pass ticket
     unsigned long long item_overflow;   // items / segments that did not fit their lists
-    unsigned long long pad[3];
+    unsigned long long posfix_fallbacks;   // coarse buckets whose position-based fix-up (K3 step 4p) left an
+                                            // inversion and went through the rank-bucket walk
+    unsigned long long pad[2];
 };
 
 // A K3 round item: the rank buckets [f_lo, f_hi) of coarse bucket c, cnt keys, sorted into the

@@ -26,6 +26,7 @@
 
 #include "k3_sort.cuh"
 #include "k3_big.cuh"
+#include "k3_posfix_net.cuh"
 
 namespace mlsort {
 
@@ -65,6 +66,7 @@ struct K3LParams {
     uint32_t item_cap;      // ITEMS pass: capacity of the item list (k3_big.cuh)
     uint32_t fshift;        // coarse-bucket passes: rank bucket = fine id >> fshift (experiments)
     uint32_t premid;        // primary pass: K2 already listed the too-large buckets (skip them)
+    uint32_t posfix;        // key-only 32-bit keys: position-based fix-up (step 4p) before the walk
 };
 
 // The rank-bucket histogram holds two u16 counters per 32-bit word (a coarse bucket never
@@ -335,6 +337,51 @@ __device__ __forceinline__ bool k3l_store_verify(const typename KeyTraits<KeyT>:
     return bad;
 }
 
+// ---- 4p. position-based fix-up (key-only, 32-bit keys).  After the placement the coarse
+// bucket is ordered by rank bucket, and for a monotone model the rank buckets are key ranges
+// (Eq. 4), so sorting ANY window of consecutive positions only reorders keys inside their rank
+// buckets.  Pass A sorts the windows [20w, 20w + 20) in registers (one window per thread,
+// 103-comparator network); pass B merges the sorted upper 8 of window w with the sorted lower 12
+// of window w + 1 (37 comparators).  A rank bucket of up to 9 keys lies inside an A window or
+// inside a B window ([20w + 12, 20w + 32)), so it ends up sorted; at one key per rank bucket on
+// average (B = N) a longer one is a 1e-7 event per bucket, and the always-on order check of
+// the store sends such a coarse bucket (and the two that hold the clamped tails) through the
+// rank-bucket walk.  No per-bucket bookkeeping: ~0.5 warp instructions per key instead of ~1.8.
+// The 80-byte thread stride makes every 128-bit shared access conflict-free (16-byte unit
+// (5l + v) mod 8 is distinct over the 8 lanes of a phase).  skey[n, 20 nw) holds 0xFFFFFFFF.
+#define MLSORT_CX(a, b) { const uint32_t lo_ = min(k[a], k[b]); k[b] = max(k[a], k[b]); k[a] = lo_; }
+template <int NT>
+__device__ __forceinline__ void k3l_posfix(uint32_t* skey, uint32_t nw) {
+    for (uint32_t w = threadIdx.x; w < nw; w += NT) {
+        uint4* p4 = reinterpret_cast<uint4*>(skey + 20u * w);
+        uint32_t k[20];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+            const uint4 q = p4[v];
+            k[4 * v] = q.x; k[4 * v + 1] = q.y; k[4 * v + 2] = q.z; k[4 * v + 3] = q.w;
+        }
+        MLSORT_SORT20(MLSORT_CX)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) p4[v] = make_uint4(k[4 * v], k[4 * v + 1], k[4 * v + 2], k[4 * v + 3]);
+    }
+    __syncthreads();
+    for (uint32_t w = threadIdx.x; w + 1u < nw; w += NT) {
+        uint4* p4 = reinterpret_cast<uint4*>(skey + 20u * w + 12u);
+        uint32_t k[20];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+            const uint4 q = p4[v];
+            k[4 * v] = q.x; k[4 * v + 1] = q.y; k[4 * v + 2] = q.z; k[4 * v + 3] = q.w;
+        }
+        MLSORT_MERGE20(MLSORT_CX)
+        constexpr int pm[20] = MLSORT_MERGE20_PERM;
+#pragma unroll
+        for (int v = 0; v < 5; ++v)
+            p4[v] = make_uint4(k[pm[4 * v]], k[pm[4 * v + 1]], k[pm[4 * v + 2]], k[pm[4 * v + 3]]);
+    }
+    __syncthreads();
+}
+
 // ITEMS = true: the round pass over the items of k3_cut (k3_big.cuh): work item t sorts the rank
 // buckets [f_lo, f_hi) of coarse bucket c -- it reads c's whole region and keeps only those --
 // into the output range starting at `out`; everything else is the same code.
@@ -551,6 +598,14 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         __syncthreads();
         prefetch_next();
         K3L_T(2);
+        // step 4p applies when the padded windows fit (skey[n, np) = +max pads the last window)
+        const uint32_t npos = ((n + 19u) / 20u) * 20u;
+        bool pos = false;
+        if constexpr (!PERM && !ITEMS && sizeof(Bits) == 4) {
+            pos = p.posfix && npos <= p.cap;
+            if (pos)
+                for (uint32_t q = n + tid; q < npos; q += NT) skey[q] = ~(Bits)0;
+        }
         // ---- 3. placement into rank-bucket order (ids + keys as 128-bit vectors)
         auto place8 = [&](uint32_t i, const uint4 fv) {
             KeyT kv[8];
@@ -591,6 +646,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         // queues (ballot + prefix) and sorted 32 at a time, one per lane, by padded 4- and
         // 8-element networks in registers; up to kL3RankMax by insertion in their own lane, longer ones
         // (tails clamped into the end buckets, heavy duplicates) queued for a block-wide sort.
+        auto walk = [&]() {
         {
             uint32_t* wq = wqueue + warp * 2 * kL3WarpQ;        // 2..4-element buckets
             uint32_t* wq8 = wq + kL3WarpQ;                      // 5..8-element buckets
@@ -655,26 +711,40 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
             }
         }
         __syncthreads();
-        K3L_T(4);
         // ---- 5. large rank buckets (tails collected in the end buckets, heavy duplicates):
         // block-wide bitonic sort in shared memory
         const uint32_t nbig = ctrl[2];
         if (nbig <= kL3BigQ)
             for (uint32_t q = 0; q < nbig; ++q) block_bitonic_sort_nt<KeyT, PERM, NT>(skey, sidx, bigq[2 * q], bigq[2 * q + 1]);
-        K3L_T(5);
-        // ---- 5b./7. coalesced store of the sorted coarse bucket to its output range, fused with
-        // the adjacent-order check of reading A14 over the WHOLE coarse bucket (every rank bucket
-        // is sorted, so only rank-bucket boundaries can be out of order).  It runs for every
-        // model: a non-monotone model, or an ulp-level non-monotone network output, then costs a
-        // re-sort of this coarse bucket in shared memory and a second store -- never a wrong
-        // output.
         if (nbig > kL3BigQ) block_bitonic_sort_nt<KeyT, PERM, NT>(skey, sidx, 0, n);
-        const bool bad = k3l_store_verify<KeyT, PERM, NT>(skey, sidx, n, out_keys + S0);
-        if (__syncthreads_or(bad)) {
-            block_bitonic_sort_nt<KeyT, PERM, NT>(skey, sidx, 0, n);
-            if (tid == 0) atomicAdd(&st->local_repairs, 1ull);
-            k3l_store<KeyT, NT>(skey, n, out_keys + S0);
+        };
+        // ---- 5b./7. coalesced store of the sorted coarse bucket to its output range, fused with
+        // the adjacent-order check of reading A14 over the WHOLE coarse bucket.  It runs for every
+        // model and every fix-up: mode 0 = step 4p done (an inversion left: a rank bucket longer
+        // than the windows guarantee -> the walk), mode 1 = the walk (an inversion left: a
+        // non-monotone model, or an ulp-level non-monotone network output -> mode 2, a re-sort of
+        // the whole coarse bucket in shared memory) -- never a wrong output.
+        int mode = 1;
+        if constexpr (!PERM && !ITEMS && sizeof(Bits) == 4) {
+            if (pos) {
+                k3l_posfix<NT>(reinterpret_cast<uint32_t*>(skey), npos / 20u);
+                mode = 0;
+            }
         }
+        K3L_T(4);
+        for (;;) {
+            if (mode == 1) {
+                walk();
+            } else if (mode == 2) {
+                block_bitonic_sort_nt<KeyT, PERM, NT>(skey, sidx, 0, n);
+                if (tid == 0) atomicAdd(&st->local_repairs, 1ull);
+            }
+            const bool bad = k3l_store_verify<KeyT, PERM, NT>(skey, sidx, n, out_keys + S0);
+            if (!__syncthreads_or(bad) || mode == 2) break;
+            if (mode == 0 && tid == 0) atomicAdd(&st->posfix_fallbacks, 1ull);
+            ++mode;
+        }
+        K3L_T(5);
         if (PERM) k3l_store<uint32_t, NT>(sidx, n, out_perm + S0);
         K3L_T(6);
     }

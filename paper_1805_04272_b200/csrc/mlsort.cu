@@ -728,6 +728,15 @@ cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_k
         const char* e = std::getenv("MLSORT_K3_FSHIFT");
         kp.fshift = e ? (uint32_t)std::atoi(e) : (p.kfine >= 4096 ? 1u : 0u);
     }
+    {   // key-only f32, primary pass, at most ~1 key per rank bucket: position-based fix-up (step 4p
+        // of k3_local.cuh) on unmerged rank buckets.  The secondary pass holds the overloaded
+        // coarse buckets (longer rank buckets) and keeps the walk.  MLSORT_K3_POSFIX=0/1 overrides.
+        const char* e = std::getenv("MLSORT_K3_POSFIX");
+        const bool fit = !PERM && !ITEMS && sizeof(KeyT) == 4 && !secondary &&
+                         (double)p.n <= 1.001 * (double)p.C * (double)p.kfine;
+        kp.posfix = (e ? std::atoi(e) != 0 : true) && fit ? 1u : 0u;
+        if (kp.posfix && !std::getenv("MLSORT_K3_FSHIFT")) kp.fshift = 0u;
+    }
     DevStatus* st = at<DevStatus>(ws, L.status);
     unsigned long long* ticket = ITEMS ? &st->ticket3d : (secondary ? &st->ticket3b : &st->ticket3);
     kern<<<grid, NT, smem, s>>>(kp, at<KeyT>(ws, L.reg_keys), at<uint16_t>(ws, L.reg_fine),
@@ -1356,9 +1365,9 @@ int run_pipeline(const KeyT* keys, uint64_t n, uint64_t B, const Weights* w, int
     }
     if (std::getenv("MLSORT_DEBUG"))
         fprintf(stderr, "mlsort: plan C=%u fb=%u R=%u local=%d ws=%d group=%d cap=%u cap1=%u | k5=%llu k3=%llu "
-                "region_overflow=%llu overflow=%llu big=%llu local_repairs=%llu -> violations=%llu\n",
+                "region_overflow=%llu overflow=%llu big=%llu local_repairs=%llu posfix_fallbacks=%llu -> violations=%llu\n",
                 p.C, p.fb, p.R, (int)p.local, (int)p.ws, (int)p.ws_group, p.cap, p.cap1, st.violations,
-                st.k3_violations, st.region_overflow, st.overflow, st.big_count, st.local_repairs,
+                st.k3_violations, st.region_overflow, st.overflow, st.big_count, st.local_repairs, st.posfix_fallbacks,
                 (unsigned long long)violations);
     if (info) info->repairs = violations + st.local_repairs;
     if (violations > 0) {   // reading A14: escalate to the conventional sort
