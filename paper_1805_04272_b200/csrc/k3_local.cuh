@@ -67,6 +67,7 @@ struct K3LParams {
     uint32_t fshift;        // coarse-bucket passes: rank bucket = fine id >> fshift (experiments)
     uint32_t premid;        // primary pass: K2 already listed the too-large buckets (skip them)
     uint32_t posfix;        // key-only 32-bit keys: position-based fix-up (step 4p) before the walk
+    uint32_t tails_first;   // primary pass: ticket 0 = coarse bucket C-1 (both tail buckets start first)
 };
 
 // The rank-bucket histogram holds two u16 counters per 32-bit word (a coarse bucket never
@@ -412,7 +413,12 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
     // k3_cut items (ITEMS)
     const uint32_t items = ITEMS ? (uint32_t)min(st->item_count, (unsigned long long)p.item_cap)
                                  : (p.secondary ? (uint32_t)st->mid_count : p.num_coarse);
-    auto coarse_of = [&](uint32_t t) { return ITEMS ? item_list[t].c : (p.secondary ? mid_list[t] : t); };
+    // primary pass: ticket 0 is the last coarse bucket, so both end buckets -- the clamped tails
+    // sit in their outer rank buckets and cost a block-wide sort -- start first instead of one of
+    // them being the kernel's tail
+    auto coarse_of = [&](uint32_t t) {
+        return ITEMS ? item_list[t].c : (p.secondary ? mid_list[t] : (p.tails_first ? (t == 0u ? p.num_coarse - 1u : t - 1u) : t));
+    };
     if (tid == 0) {
         const uint32_t t0 = (uint32_t)atomicAdd(ticket, 1ull);
         ctrl[1] = t0;

@@ -729,12 +729,15 @@ cudaError_t launch_k3_pass(const Plan& p, void* ws, const Layout& L, KeyT* out_k
         kp.fshift = e ? (uint32_t)std::atoi(e) : (p.kfine >= 4096 ? 1u : 0u);
     }
     {   // key-only f32, primary pass, at most ~1 key per rank bucket: position-based fix-up (step 4p
-        // of k3_local.cuh) on unmerged rank buckets.  The secondary pass holds the overloaded
-        // coarse buckets (longer rank buckets) and keeps the walk.  MLSORT_K3_POSFIX=0/1 overrides.
+        // of k3_local.cuh) on unmerged rank buckets, in both passes (the secondary pass holds the
+        // overloaded coarse buckets, whose longer rank buckets fall back to the walk more often;
+        // still faster: profiles/r02/ab_k3_posfix.log).  MLSORT_K3_POSFIX=0/1/2 overrides.
         const char* e = std::getenv("MLSORT_K3_POSFIX");
-        const bool fit = !PERM && !ITEMS && sizeof(KeyT) == 4 && !secondary &&
+        const bool fit = !PERM && !ITEMS && sizeof(KeyT) == 4 &&
                          (double)p.n <= 1.001 * (double)p.C * (double)p.kfine;
-        kp.posfix = (e ? std::atoi(e) != 0 : true) && fit ? 1u : 0u;
+        const int pv = e ? std::atoi(e) : 2;       // 1: the primary pass only (experiments)
+        kp.posfix = fit && (pv >= 2 || (pv == 1 && !secondary)) ? 1u : 0u;
+        kp.tails_first = !ITEMS && !secondary && !std::getenv("MLSORT_K3_NO_TAILS_FIRST") ? 1u : 0u;
         if (kp.posfix && !std::getenv("MLSORT_K3_FSHIFT")) kp.fshift = 0u;
     }
     DevStatus* st = at<DevStatus>(ws, L.status);
