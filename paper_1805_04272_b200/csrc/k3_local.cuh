@@ -292,6 +292,56 @@ __device__ __forceinline__ bool k3l_store_verify(const typename KeyTraits<KeyT>:
     }
     const uint32_t nv = (n - head) / V;
     KeyT* o = out + head;
+    // key-only, src + head 16-B aligned (the kernel shifts the array by the output's
+    // misalignment): one 128-bit shared load per vector, the predecessor from the lane below
+    if (!PERM && ((uint32_t)reinterpret_cast<uintptr_t>(src + head) & 15u) == 0u) {
+        const uint32_t lane = threadIdx.x & 31u;
+        for (uint32_t vb = threadIdx.x - lane; vb < nv; vb += NT) {      // warp-uniform trip count
+            const uint32_t v = vb + lane;
+            const bool ok = v < nv;
+            const uint32_t i0 = head + V * v;
+            Bits c[V];
+            if (ok) {
+                if constexpr (V == 4) {
+                    const uint4 t = *reinterpret_cast<const uint4*>(src + i0);
+                    c[0] = (Bits)t.x; c[1] = (Bits)t.y; c[2] = (Bits)t.z; c[V - 1] = (Bits)t.w;
+                } else {
+                    const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(src + i0);
+                    c[0] = (Bits)t.x; c[V - 1] = (Bits)t.y;
+                }
+            } else {
+#pragma unroll
+                for (uint32_t q = 0; q < V; ++q) c[q] = (Bits)0;
+            }
+            Bits prev = __shfl_up_sync(0xffffffffu, c[V - 1], 1);
+            if (lane == 0u && ok) prev = i0 ? src[i0 - 1] : c[0];
+            if (!ok) continue;
+#pragma unroll
+            for (uint32_t q = 0; q < V; ++q) {
+                bad |= c[q] < prev;
+                prev = c[q];
+            }
+            if (V == 4) {
+                float4 qv;
+                uint32_t* qq = reinterpret_cast<uint32_t*>(&qv);
+#pragma unroll
+                for (uint32_t q = 0; q < V; ++q) {
+                    const KeyT t = K3Out<KeyT>::conv(c[q]);
+                    qq[q] = *reinterpret_cast<const uint32_t*>(&t);
+                }
+                __stcs(reinterpret_cast<float4*>(o) + v, qv);
+            } else {
+                double2 qv;
+                unsigned long long* qq = reinterpret_cast<unsigned long long*>(&qv);
+#pragma unroll
+                for (uint32_t q = 0; q < V; ++q) {
+                    const KeyT t = K3Out<KeyT>::conv(c[q]);
+                    qq[q] = *reinterpret_cast<const unsigned long long*>(&t);
+                }
+                __stcs(reinterpret_cast<double2*>(o) + v, qv);
+            }
+        }
+    } else
     for (uint32_t v = threadIdx.x; v < nv; v += NT) {
         const uint32_t i0 = head + V * v;
         Bits c[V];
@@ -404,8 +454,8 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
     uint32_t* bigq = ctrl + 80;
     uint32_t* wqueue = reinterpret_cast<uint32_t*>(smem + kCtrlBytes);
     uint32_t* h2 = reinterpret_cast<uint32_t*>(smem + kCtrlBytes + k3l_queue_bytes(NT));   // u16 counter pairs
-    Bits* skey = reinterpret_cast<Bits*>(h2 + k3l_hist_words(p.kfine));
-    uint32_t* sidx = reinterpret_cast<uint32_t*>(skey + p.cap);
+    Bits* skey0 = reinterpret_cast<Bits*>(h2 + k3l_hist_words(p.kfine));      // 16-B aligned
+    uint32_t* sidx = reinterpret_cast<uint32_t*>(skey0 + p.cap);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (st->region_overflow) return;       // K1 overflowed a region: incomplete regions, re-run follows
@@ -557,7 +607,10 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         // (128-bit loads, WPT a multiple of 4) in registers, then one block-wide scan of the
         // per-thread totals
         {
-            const uint32_t wpt = (((hwp + NT - 1) / NT) + 3u) & ~3u;
+            // (an ODD number of 16-byte vectors per thread: the lane stride is then an odd multiple
+            // of 16 B and the 128-bit accesses are bank-conflict-free; 4 vectors per thread were
+            // 4-way conflicts, 12.6 M of the 56.7 M shared wavefronts of C2's K3)
+            const uint32_t wpt = (((((hwp + NT - 1) / NT) + 3u) >> 2) | 1u) << 2;
             const uint32_t tw0 = min(hwp, (uint32_t)tid * wpt), tw1 = min(hwp, tw0 + wpt);
             uint4* h8 = reinterpret_cast<uint4*>(h2);
             uint32_t tot = 0;
@@ -604,13 +657,24 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         __syncthreads();
         prefetch_next();
         K3L_T(2);
-        // step 4p applies when the padded windows fit (skey[n, np) = +max pads the last window)
-        const uint32_t npos = ((n + 19u) / 20u) * 20u;
+        // The sorted keys start `off` elements into the 16-B aligned array, off = the output
+        // range's misalignment, so the store reads shared memory and writes global memory with
+        // 128-bit accesses at the same element (scalar 4-byte shared loads at a 16-byte lane
+        // stride were 4-way bank conflicts: 10.5 M of the 56.7 M shared wavefronts of C2's K3).
+        constexpr uint32_t kVec = 16u / (uint32_t)sizeof(KeyT);
+        uint32_t off = (uint32_t)(reinterpret_cast<uintptr_t>(out_keys + S0) / sizeof(KeyT)) & (kVec - 1u);
+        if (n + off > p.cap) off = 0u;
+        Bits* skey = skey0 + off;
+        // step 4p works on the physical array skey0[0, npos): `off` minimum pads in front, the
+        // keys, maximum pads up to the last window's end; it applies when that fits
+        const uint32_t npos = ((off + n + 19u) / 20u) * 20u;
         bool pos = false;
         if constexpr (!PERM && !ITEMS && sizeof(Bits) == 4) {
             pos = p.posfix && npos <= p.cap;
-            if (pos)
-                for (uint32_t q = n + tid; q < npos; q += NT) skey[q] = ~(Bits)0;
+            if (pos) {
+                if (tid < off) skey0[tid] = (Bits)0;
+                for (uint32_t q = off + n + tid; q < npos; q += NT) skey0[q] = ~(Bits)0;
+            }
         }
         // ---- 3. placement into rank-bucket order (ids + keys as 128-bit vectors)
         auto place8 = [&](uint32_t i, const uint4 fv) {
@@ -733,7 +797,7 @@ k3_local_sort(K3LParams p, const KeyT* __restrict__ reg_keys, const uint16_t* __
         int mode = 1;
         if constexpr (!PERM && !ITEMS && sizeof(Bits) == 4) {
             if (pos) {
-                k3l_posfix<NT>(reinterpret_cast<uint32_t*>(skey), npos / 20u);
+                k3l_posfix<NT>(reinterpret_cast<uint32_t*>(skey0), npos / 20u);
                 mode = 0;
             }
         }
