@@ -10,6 +10,9 @@
 //      unsigned key bits; index alongside for perm sorts)                            -- A5
 //   4. fix-up in place: rank buckets of 2-8 elements by register sorting networks, up to 24 by
 //      insertion, larger ones by a block bitonic sort                                  -- A6
+//   4p. key-only 32-bit keys at <= 1 key per rank bucket (C2): position-based fix-up instead --
+//      two passes of 20-key window sorts over the placed array (k3l_posfix); the order check
+//      of step 5 sends a coarse bucket it leaves unsorted through step 4               -- A6
 //   5. the store is fused with an adjacent-order check of the whole coarse bucket; an
 //      inversion (non-monotone model or float effects) re-sorts it in smem  -- A7 (A14)
 // The primary pass runs two 512-thread CTAs per SM (two coarse buckets in flight hide each

@@ -93,6 +93,25 @@ def test_sort_all_equal_and_grid_duplicates(mls):
     check_sort(mls, keys, w, p, perm=False)
 
 
+@pytest.mark.parametrize("rep", [1, 4, 9, 10, 16, 48])
+def test_sort_keyonly_position_fixup(mls, rep):
+    """K3 step 4p (key-only f32, B = N): rank buckets that hold `rep` DISTINCT keys a few ulps
+    apart.  Up to 9 are sorted by the two window passes; longer ones are beyond the windows'
+    guarantee, the store's order check must catch them and the walk must sort them
+    (K3 step 4p).  n is odd, so output ranges start at every misalignment."""
+    n = (1 << 20) + 77
+    base = workloads.generate("normal", n // rep + 1, 21, "f32")
+    bits = np.repeat(base.view(np.uint32), rep)[:n].astype(np.int64)
+    jit = np.tile(np.arange(rep, dtype=np.int64), n // rep + 1)[:n]
+    bits = np.where(bits & 0x80000000, bits - jit, bits + jit)      # |key| grows by jit ulps
+    keys = bits.astype(np.uint32).view(np.float32).copy()
+    assert np.isfinite(keys).all()
+    np.random.default_rng(5).shuffle(keys)
+    w, p = _fit(mls, keys, 32, n0=1 << 14)
+    info, _ = check_sort(mls, keys, w, p, perm=False)
+    assert info["fallback_used"] == 0
+
+
 def test_sort_degenerate_w2_zero(mls):
     keys = workloads.generate("normal", 100000, 9, "f32")
     w = mls.Weights.create(1, [1.0], [0.0], [0.0], [1.0], -3.0, 3.0)   # S:116: every key -> bucket 0
