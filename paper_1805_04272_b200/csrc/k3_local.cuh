@@ -295,6 +295,15 @@ __device__ __forceinline__ bool k3l_store_verify(const typename KeyTraits<KeyT>:
     }
     const uint32_t nv = (n - head) / V;
     KeyT* o = out + head;
+    auto tail = [&](bool b) {                  // the elements behind the last whole vector
+        bad = b;
+        for (uint32_t i = head + nv * V + threadIdx.x; i < n; i += NT) {
+            const Bits c = src[i];
+            chk(i, c);
+            out[i] = K3Out<KeyT>::conv(c);
+        }
+        return bad;
+    };
     // key-only, src + head 16-B aligned (the kernel shifts the array by the output's
     // misalignment): one 128-bit shared load per vector, the predecessor from the lane below
     if (!PERM && ((uint32_t)reinterpret_cast<uintptr_t>(src + head) & 15u) == 0u) {
@@ -344,7 +353,8 @@ __device__ __forceinline__ bool k3l_store_verify(const typename KeyTraits<KeyT>:
                 __stcs(reinterpret_cast<double2*>(o) + v, qv);
             }
         }
-    } else
+        return tail(bad);
+    }
     for (uint32_t v = threadIdx.x; v < nv; v += NT) {
         const uint32_t i0 = head + V * v;
         Bits c[V];
@@ -383,12 +393,7 @@ __device__ __forceinline__ bool k3l_store_verify(const typename KeyTraits<KeyT>:
             __stcs(reinterpret_cast<double2*>(o) + v, qv);
         }
     }
-    for (uint32_t i = head + nv * V + threadIdx.x; i < n; i += NT) {
-        const Bits c = src[i];
-        chk(i, c);
-        out[i] = K3Out<KeyT>::conv(c);
-    }
-    return bad;
+    return tail(bad);
 }
 
 // ---- 4p. position-based fix-up (key-only, 32-bit keys).  After the placement the coarse
